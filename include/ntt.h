@@ -1,0 +1,142 @@
+/*
+ * include/ntt.h -- C ABI of libntt.so: the batched merged-negacyclic NTT / iNTT
+ * over RNS residue rows on NVIDIA B200 (sm_100a).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n (arxiv 2012.01968);
+ * "R#" = the readings of silent/garbled passages in DESIGN.md section 3.
+ *
+ * General rules (all entry points):
+ *  - No C++ type, exception or torch type crosses this boundary.  Pointers are
+ *    plain host or device pointers as stated per argument; sizes are unsigned.
+ *  - Every function returns an ntt_status_t.  Argument errors are detected
+ *    synchronously, before anything is enqueued, and leave all buffers
+ *    untouched.  A CUDA launch failure is reported as NTT_ERR_CUDA (from
+ *    cudaPeekAtLastError); asynchronous faults surface at the caller's next
+ *    synchronisation, as for any CUDA library.
+ *  - A plan is immutable after ntt_plan_create; concurrent ntt_forward /
+ *    ntt_inverse calls with one plan on different streams and disjoint buffers
+ *    are safe.  ntt_plan_destroy requires all work using the plan to be done.
+ *  - There is no CPU fallback: without a usable CUDA device ntt_plan_create
+ *    returns NTT_ERR_CUDA.
+ */
+#ifndef NTT_B200_H
+#define NTT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ntt_plan_s *ntt_plan_t;
+
+typedef enum {
+    NTT_OK = 0,
+    NTT_ERR_INVALID_N = -1,       /* N not a power of two in [2^1, 2^17] */
+    NTT_ERR_INVALID_PRIME = -2,   /* not prime, not = 1 mod 2N, >= 2^60, or repeated */
+    NTT_ERR_INVALID_ARG = -3,     /* null pointer, bad option value */
+    NTT_ERR_MISALIGNED = -4,      /* data pointer not 16-byte aligned */
+    NTT_ERR_WRONG_DEVICE = -5,    /* data pointer not on the plan's device */
+    NTT_ERR_CUDA = -6,            /* CUDA runtime error (no device, launch failure) */
+    NTT_ERR_OOM = -7,             /* device or pinned allocation failed */
+    NTT_ERR_RANGE_EXHAUSTED = -8  /* fewer primes than requested in [2^59, 2^60) */
+} ntt_status_t;
+
+/* Options; a zero field means "default". */
+typedef struct {
+    int ot_enable;       /* on-the-fly twiddling in the last ot_stages
+                            forward stages and the first ot_stages inverse stages:
+                            0 = default (off), 1 = on, -1 = off */
+    unsigned ot_base;    /* OT base B, power of two dividing N;
+                            0 = 1024 for N >= 2^11, else 2^ceil(logN/2) (R11) */
+    unsigned ot_stages;  /* 1 or 2 (fig:3point c); 0 = 2 */
+    unsigned log_n1;     /* two-kernel split N = N1*N2, log2 N1;
+                            0 = automatic; ignored when one kernel holds the row */
+} ntt_opts_t;
+
+/* ntt_find_primes -- host helper, no device needed.
+ * Writes the first `count` primes p = 1 (mod 2N), 2^59 <= p < 2^60, scanning
+ * downward from 2^60 - 2N + 1 (R1, R3) into out[0..count).
+ * Deterministic.  n = N (power of two, 2 <= N <= 2^17).
+ * Errors: INVALID_N, INVALID_ARG (out == NULL or count == 0), RANGE_EXHAUSTED. */
+ntt_status_t ntt_find_primes(unsigned n, unsigned count, uint64_t *out);
+
+/* ntt_find_psi -- host helper.  The smallest primitive 2N-th root of unity mod
+ * p (psi^N = -1; R2) into *psi.  Errors: INVALID_N, INVALID_PRIME. */
+ntt_status_t ntt_find_psi(uint64_t p, unsigned n, uint64_t *psi);
+
+/* ntt_plan_create / _ex -- build a plan for ring degree n = N and the RNS
+ * chain primes[0..L).  Copies primes[].  On the device current at
+ * the call it allocates and fills, per prime and direction, the bit-reversed
+ * twiddle table Psi[i] = psi^bitrev(i) resp.
+ * Psi^-1[i] = psi^-bitrev(i) (R5) with Shoup companions
+ * w_bar = floor(w 2^64 / p) (Algorithm 4; R6), the OT base tables
+ * fine[r] = psi^r, coarse[q] = psi^(qB) and their inverses, and
+ * N^-1.  The plan owns these allocations.  Synchronous.
+ * Errors: INVALID_ARG (plan == NULL, primes == NULL, L == 0, bad options),
+ * INVALID_N, INVALID_PRIME, CUDA (no device), OOM. */
+ntt_status_t ntt_plan_create(ntt_plan_t *plan, unsigned n, const uint64_t *primes, unsigned L);
+ntt_status_t ntt_plan_create_ex(ntt_plan_t *plan, unsigned n, const uint64_t *primes, unsigned L,
+                                const ntt_opts_t *opts);
+
+/* ntt_plan_psi -- copies the plan's psi for each prime into psi_out[0..L)
+ * (host memory), so tests can assert the oracle picked the same root. */
+ntt_status_t ntt_plan_psi(ntt_plan_t plan, uint64_t *psi_out);
+
+/* ntt_plan_info -- host query: L, log2 N, log2 N1 of the split actually used
+ * (0 when one kernel holds the whole row), OT on/off, OT base, OT stages,
+ * and device-table bytes.  Any output pointer may be NULL. */
+ntt_status_t ntt_plan_info(ntt_plan_t plan, unsigned *L, unsigned *logn, unsigned *log_n1,
+                           int *ot_enable, unsigned *ot_base, unsigned *ot_stages,
+                           uint64_t *table_bytes);
+
+/* ntt_forward -- in-place forward merged negacyclic NTT of batch*L rows.
+ *   data: DEVICE pointer on the plan's device, 16-byte aligned, to
+ *         batch x L x N uint64 words, row-major [b][l][i]; row (b, l) holds a
+ *         polynomial with coefficients in [0, primes[l]) (precondition, not
+ *         checked on the device; out-of-range input gives an undefined result).
+ *   On completion position i of a row holds A_{bitrev(i)} with
+ *   A_k = sum_j a_j psi^{j(2k+1)} mod p (bit-reversed order P:298; R4),
+ *   canonical in [0, p) (R10).
+ *   stream: a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   Asynchronous: returns after enqueuing.  batch == 0 is a no-op (NTT_OK).
+ *   Errors: INVALID_ARG (plan/data NULL), MISALIGNED, WRONG_DEVICE, CUDA. */
+ntt_status_t ntt_forward(ntt_plan_t plan, uint64_t *data, unsigned batch, void *stream);
+
+/* ntt_inverse -- in-place inverse: bit-reversed NTT-domain rows in [0, p) to
+ * natural-order coefficients c_k = N^-1 sum_n C_n psi^{-k(2n+1)} (
+ * R5, R15), canonical in [0, p).  ntt_inverse(ntt_forward(x)) == x exactly.
+ * Same arguments, layout, ownership and errors as ntt_forward. */
+ntt_status_t ntt_inverse(ntt_plan_t plan, uint64_t *data, unsigned batch, void *stream);
+
+/* ntt_execute_host -- the end-to-end path with HOST buffers: for each chunk of
+ * ciphertexts, copy host_in -> device workspace, run the requested transforms
+ * (flags: NTT_DIR_FORWARD, NTT_DIR_INVERSE, or both = forward then inverse),
+ * copy back to host_out (may equal host_in).  Chunks are pipelined over two
+ * internal streams so H2D, kernels and D2H overlap.
+ *   host_in/host_out: HOST pointers to batch x L x N words (pinned memory gives
+ *   overlap; pageable memory works but serialises).
+ *   workspace: DEVICE pointer on the plan's device, 16-byte aligned, of at
+ *   least ntt_workspace_words(plan, chunk) words; chunk = ciphertexts per
+ *   pipeline step (0 = automatic).
+ *   Synchronous: returns when host_out holds the result.
+ *   Errors: as ntt_forward, plus INVALID_ARG for a too-small workspace. */
+#define NTT_DIR_FORWARD 1u
+#define NTT_DIR_INVERSE 2u
+ntt_status_t ntt_execute_host(ntt_plan_t plan, unsigned flags, const uint64_t *host_in, uint64_t *host_out,
+                              unsigned batch, uint64_t *workspace, uint64_t workspace_words, unsigned chunk);
+
+/* Words of device workspace ntt_execute_host needs for a given chunk (0 = auto). */
+uint64_t ntt_workspace_words(ntt_plan_t plan, unsigned batch, unsigned chunk);
+
+/* ntt_plan_destroy -- frees the plan's device tables and host state.
+ * NULL is accepted (no-op).  Caller must have synchronised all work. */
+ntt_status_t ntt_plan_destroy(ntt_plan_t plan);
+
+/* Static English text for a status code. */
+const char *ntt_status_string(ntt_status_t s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NTT_B200_H */

@@ -1,0 +1,156 @@
+// tools/alu_roof.cu -- integer-pipe micro-benchmark for the NTT's ALU roof
+// (SURVEY section 7 step 0).  Measures per-SM throughput of the instructions a
+// 64-bit Shoup butterfly is made of, and of whole butterflies, with every
+// thread running independent chains so only pipe throughput limits.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/alu_roof tools/alu_roof.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define CH 8
+#define ITERS 2048
+
+__global__ void k_imad_wide(uint64_t* out, uint32_t a, uint32_t b) {
+  uint64_t acc[CH];
+  for (int c = 0; c < CH; ++c) acc[c] = threadIdx.x + c;
+  uint32_t x = a ^ threadIdx.x, y = b;
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      asm volatile("{ .reg .u32 lo, hi; mov.b64 {lo, hi}, %0; mad.wide.u32 %0, lo, %1, %0; }" : "+l"(acc[c]) : "r"(x + c));
+  uint64_t s = 0;
+  for (int c = 0; c < CH; ++c) s ^= acc[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_imad(uint64_t* out, uint32_t a, uint32_t b) {
+  uint32_t acc[CH];
+  for (int c = 0; c < CH; ++c) acc[c] = threadIdx.x + c;
+  uint32_t x = a ^ threadIdx.x, y = b;
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(acc[c]) : "r"(x), "r"(y + c));
+  uint32_t s = 0;
+  for (int c = 0; c < CH; ++c) s ^= acc[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_imad_hi(uint64_t* out, uint32_t a, uint32_t b) {
+  uint32_t acc[CH];
+  for (int c = 0; c < CH; ++c) acc[c] = threadIdx.x + c;
+  uint32_t x = a ^ threadIdx.x, y = b;
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(acc[c]) : "r"(x), "r"(y + c));
+  uint32_t s = 0;
+  for (int c = 0; c < CH; ++c) s ^= acc[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_iadd3(uint64_t* out, uint32_t a, uint32_t b) {
+  uint32_t acc[CH];
+  for (int c = 0; c < CH; ++c) acc[c] = threadIdx.x + c;
+  uint32_t x = a ^ threadIdx.x, y = b;
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      asm volatile("add.u32 %0, %0, %1;" : "+r"(acc[c]) : "r"(x + c));
+  uint32_t s = 0;
+  for (int c = 0; c < CH; ++c) s ^= acc[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_mix(uint64_t* out, uint32_t a, uint32_t b) {  // 1 IMAD : 1 IADD
+  uint32_t acc[CH], acc2[CH];
+  for (int c = 0; c < CH; ++c) { acc[c] = threadIdx.x + c; acc2[c] = c; }
+  uint32_t x = a ^ threadIdx.x, y = b;
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(acc[c]) : "r"(x), "r"(y + c));
+      asm volatile("add.u32 %0, %0, %1;" : "+r"(acc2[c]) : "r"(x + c));
+    }
+  uint32_t s = 0;
+  for (int c = 0; c < CH; ++c) s ^= acc[c] ^ acc2[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__device__ __forceinline__ uint64_t shoup_lazy(uint64_t b, uint64_t w, uint64_t wb, uint64_t p) {
+  return b * w - __umul64hi(b, wb) * p;
+}
+// Harvey CT butterfly, inputs/outputs < 4p
+__global__ void k_bf_ct(uint64_t* out, uint64_t p, uint64_t w, uint64_t wb) {
+  uint64_t X[CH], Y[CH];
+  for (int c = 0; c < CH; ++c) { X[c] = (threadIdx.x * 77 + c) % p; Y[c] = (threadIdx.x * 31 + c * 5) % p; }
+  const uint64_t p2 = 2 * p;
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      uint64_t x = X[c] >= p2 ? X[c] - p2 : X[c];
+      uint64_t t = shoup_lazy(Y[c], w, wb, p);
+      X[c] = x + t;
+      Y[c] = x - t + p2;
+    }
+  uint64_t s = 0;
+  for (int c = 0; c < CH; ++c) s ^= X[c] ^ Y[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+// Shoup lazy multiply alone (chained)
+__global__ void k_shoup(uint64_t* out, uint64_t p, uint64_t w, uint64_t wb) {
+  uint64_t X[CH];
+  for (int c = 0; c < CH; ++c) X[c] = (threadIdx.x * 77 + c) % p;
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) X[c] = shoup_lazy(X[c], w, wb, p);
+  uint64_t s = 0;
+  for (int c = 0; c < CH; ++c) s ^= X[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+typedef void (*kfun32)(uint64_t*, uint32_t, uint32_t);
+typedef void (*kfun64)(uint64_t*, uint64_t, uint64_t, uint64_t);
+
+int main() {
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, 0);
+  int sms = prop.multiProcessorCount;
+  int clk_khz = 0;
+  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+  printf("{\"device\": \"%s\", \"sms\": %d, \"clock_attr_mhz\": %.0f}\n", prop.name, sms, clk_khz / 1e3);
+  uint64_t* out;
+  int threads = 256, blocks_per_sm = 8;
+  int blocks = sms * blocks_per_sm;
+  cudaMalloc(&out, sizeof(uint64_t) * blocks * threads);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  struct { const char* name; kfun32 f; double ops_per_inner; } k32[] = {
+      {"mad.wide.u32", k_imad_wide, 1}, {"mad.lo.u32", k_imad, 1}, {"mad.hi.u32", k_imad_hi, 1},
+      {"add.u32", k_iadd3, 1}, {"mad.lo+add", k_mix, 2}};
+  for (auto& k : k32) {
+    for (int rep = 0; rep < 3; ++rep) k.f<<<blocks, threads>>>(out, 3, 5);
+    cudaEventRecord(e0);
+    k.f<<<blocks, threads>>>(out, 3, 5);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double ops = (double)blocks * threads * ITERS * CH * k.ops_per_inner;
+    printf("{\"kernel\": \"%s\", \"ms\": %.4f, \"Gops_per_s\": %.1f, \"ops_per_ns_per_sm\": %.3f}\n", k.name, ms,
+           ops / ms / 1e6, ops / ms / 1e6 / sms);
+  }
+  uint64_t p = 1152921504606584833ull, w = 30403152079314ull;
+  uint64_t wb = (uint64_t)(((unsigned __int128)w << 64) / p);
+  struct { const char* name; kfun64 f; } k64[] = {{"butterfly_ct_harvey", k_bf_ct}, {"shoup_lazy", k_shoup}};
+  for (auto& k : k64) {
+    for (int rep = 0; rep < 3; ++rep) k.f<<<blocks, threads>>>(out, p, w, wb);
+    cudaEventRecord(e0);
+    k.f<<<blocks, threads>>>(out, p, w, wb);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double ops = (double)blocks * threads * ITERS * CH;
+    printf("{\"kernel\": \"%s\", \"ms\": %.4f, \"Gops_per_s\": %.1f, \"ops_per_ns_per_sm\": %.3f}\n", k.name, ms,
+           ops / ms / 1e6, ops / ms / 1e6 / sms);
+  }
+  return 0;
+}
