@@ -30,6 +30,9 @@ extern "C" {
 
 typedef struct ntt_plan_s *ntt_plan_t;
 
+#define NTT_DIR_FORWARD 1u
+#define NTT_DIR_INVERSE 2u
+
 typedef enum {
     NTT_OK = 0,
     NTT_ERR_INVALID_N = -1,       /* N not a power of two in [2^1, 2^17] */
@@ -109,6 +112,18 @@ ntt_status_t ntt_forward(ntt_plan_t plan, uint64_t *data, unsigned batch, void *
  * Same arguments, layout, ownership and errors as ntt_forward. */
 ntt_status_t ntt_inverse(ntt_plan_t plan, uint64_t *data, unsigned batch, void *stream);
 
+/* ntt_launch_pass -- enqueue ONE kernel of a direction, for per-kernel timing
+ * (bench.py brackets each with CUDA events).  dir: NTT_DIR_FORWARD or
+ * NTT_DIR_INVERSE; pass: 0 or 1 in execution order.  Two-kernel plans
+ * (ntt_plan_info log_n1 != 0) have passes 0 and 1 -- forward: Kernel-1
+ * (columns) then Kernel-2 (blocks); inverse: Kernel-2' then Kernel-1' -- and
+ * ntt_forward == pass 0 then pass 1 on one stream; single-kernel plans have
+ * pass 0 only.  Same data contract as ntt_forward; the intermediate state
+ * between passes is defined only for the pass sequence.
+ * Errors: as ntt_forward, plus INVALID_ARG for a pass the plan lacks. */
+ntt_status_t ntt_launch_pass(ntt_plan_t plan, uint64_t *data, unsigned batch, unsigned dir, unsigned pass,
+                             void *stream);
+
 /* ntt_execute_host -- the end-to-end path with HOST buffers: for each chunk of
  * ciphertexts, copy host_in -> device workspace, run the requested transforms
  * (flags: NTT_DIR_FORWARD, NTT_DIR_INVERSE, or both = forward then inverse),
@@ -121,8 +136,6 @@ ntt_status_t ntt_inverse(ntt_plan_t plan, uint64_t *data, unsigned batch, void *
  *   pipeline step (0 = automatic).
  *   Synchronous: returns when host_out holds the result.
  *   Errors: as ntt_forward, plus INVALID_ARG for a too-small workspace. */
-#define NTT_DIR_FORWARD 1u
-#define NTT_DIR_INVERSE 2u
 ntt_status_t ntt_execute_host(ntt_plan_t plan, unsigned flags, const uint64_t *host_in, uint64_t *host_out,
                               unsigned batch, uint64_t *workspace, uint64_t workspace_words, unsigned chunk);
 

@@ -1,0 +1,158 @@
+"""B200-native batched negacyclic NTT / iNTT over RNS residue rows
+(arxiv 2012.01968 hot path).
+
+Thin Python layer over the C ABI in include/ntt.h (libntt.so).  PyTorch is
+used only for device memory and streams; every arithmetic step runs in the
+sm_100a kernels.  Layout of a batch: ``[batch][L][N]`` uint64 (or int64 with
+the same bits), row (b, l) reduced mod ``primes[l]``.
+
+    plan = Plan(1 << 17, find_primes(1 << 17, 60))
+    plan.forward(x)   # in place, bit-reversed NTT domain
+    plan.inverse(x)   # in place, back to coefficients
+"""
+from __future__ import annotations
+
+import ctypes
+
+from ._native import NTT_DIR_FORWARD, NTT_DIR_INVERSE, NttError, Opts, check, lib
+
+__all__ = ["Plan", "find_primes", "find_psi", "NttError", "NTT_DIR_FORWARD", "NTT_DIR_INVERSE"]
+
+
+def find_primes(N: int, count: int) -> list[int]:
+    """First ``count`` primes p = 1 mod 2N in [2^59, 2^60), descending (host)."""
+    out = (ctypes.c_uint64 * count)()
+    check(lib().ntt_find_primes(N, count, out), "ntt_find_primes")
+    return [int(v) for v in out]
+
+
+def find_psi(p: int, N: int) -> int:
+    """Smallest primitive 2N-th root of unity mod p (host)."""
+    v = ctypes.c_uint64()
+    check(lib().ntt_find_psi(p, N, ctypes.byref(v)), "ntt_find_psi")
+    return int(v.value)
+
+
+def _dev_ptr(t, N: int, L: int) -> tuple[int, int]:
+    """(data_ptr, batch) of a CUDA [batch][L][N] 64-bit tensor."""
+    import torch
+
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("expected a torch CUDA tensor")
+    if t.dtype not in (torch.uint64, torch.int64):
+        raise TypeError(f"dtype must be uint64 or int64, got {t.dtype}")
+    if not t.is_cuda:
+        raise ValueError("tensor must be on a CUDA device (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    if t.numel() % (N * L):
+        raise ValueError(f"numel {t.numel()} is not a multiple of L*N = {L * N}")
+    return t.data_ptr(), t.numel() // (N * L)
+
+
+def _stream_handle(stream) -> int:
+    import torch
+
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+class Plan:
+    """Owns the device twiddle tables of one (N, prime chain) on the current
+    CUDA device (ntt_plan_create_ex)."""
+
+    def __init__(self, N: int, primes, ot: bool = False, ot_base: int = 0, ot_stages: int = 0,
+                 log_n1: int = 0):
+        self.N = int(N)
+        self.primes = [int(p) for p in primes]
+        self.L = len(self.primes)
+        arr = (ctypes.c_uint64 * max(self.L, 1))(*self.primes)
+        opts = Opts(1 if ot else -1, ot_base, ot_stages, log_n1)
+        h = ctypes.c_void_p()
+        check(lib().ntt_plan_create_ex(ctypes.byref(h), self.N, arr, self.L, ctypes.byref(opts)),
+              "ntt_plan_create")
+        self._h = h
+
+    # ---------------------------------------------------------------- queries
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        if self._h is None:
+            raise ValueError("plan destroyed")
+        return self._h
+
+    @property
+    def psis(self) -> list[int]:
+        out = (ctypes.c_uint64 * self.L)()
+        check(lib().ntt_plan_psi(self.handle, out), "ntt_plan_psi")
+        return [int(v) for v in out]
+
+    def info(self) -> dict:
+        L, logn, logn1, ots, otb = (ctypes.c_uint() for _ in range(5))
+        ote = ctypes.c_int()
+        tb = ctypes.c_uint64()
+        check(lib().ntt_plan_info(self.handle, ctypes.byref(L), ctypes.byref(logn), ctypes.byref(logn1),
+                                  ctypes.byref(ote), ctypes.byref(otb), ctypes.byref(ots), ctypes.byref(tb)))
+        return {"L": L.value, "logn": logn.value, "log_n1": logn1.value, "ot_enable": bool(ote.value),
+                "ot_base": otb.value, "ot_stages": ots.value, "table_bytes": tb.value}
+
+    # ---------------------------------------------------------------- transforms
+    def forward(self, x, stream=None):
+        """In-place forward NTT of a CUDA [batch][L][N] tensor (asynchronous)."""
+        ptr, batch = _dev_ptr(x, self.N, self.L)
+        check(lib().ntt_forward(self.handle, ptr, batch, _stream_handle(stream)), "ntt_forward")
+        return x
+
+    def inverse(self, x, stream=None):
+        """In-place inverse NTT of a CUDA [batch][L][N] tensor (asynchronous)."""
+        ptr, batch = _dev_ptr(x, self.N, self.L)
+        check(lib().ntt_inverse(self.handle, ptr, batch, _stream_handle(stream)), "ntt_inverse")
+        return x
+
+    @property
+    def passes(self) -> int:
+        """Kernels per direction: 2 for the two-kernel split, 1 otherwise."""
+        return 2 if self.info()["log_n1"] else 1
+
+    def launch_pass(self, x, direction: int, pass_index: int, stream=None):
+        """Enqueue one kernel of a direction (for per-kernel timing)."""
+        ptr, batch = _dev_ptr(x, self.N, self.L)
+        check(lib().ntt_launch_pass(self.handle, ptr, batch, direction, pass_index, _stream_handle(stream)),
+              "ntt_launch_pass")
+        return x
+
+    def workspace_words(self, batch: int, chunk: int = 0) -> int:
+        return int(lib().ntt_workspace_words(self.handle, batch, chunk))
+
+    def execute_host(self, host_in, host_out, flags: int, workspace, chunk: int = 0) -> None:
+        """End-to-end transform of HOST buffers (numpy arrays or CPU tensors,
+        ideally pinned) through a device workspace; synchronous."""
+        def hptr(a):
+            if hasattr(a, "data_ptr"):
+                return a.data_ptr(), a.numel()
+            return a.ctypes.data, a.size
+        pin, n_in = hptr(host_in)
+        pout, n_out = hptr(host_out)
+        if n_in != n_out or n_in % (self.N * self.L):
+            raise ValueError("host buffers must both hold batch*L*N words")
+        wptr = workspace.data_ptr()
+        check(lib().ntt_execute_host(self.handle, flags, pin, pout, n_in // (self.N * self.L), wptr,
+                                     workspace.numel(), chunk), "ntt_execute_host")
+
+    # ---------------------------------------------------------------- lifetime
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None:
+            lib().ntt_plan_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,81 @@
+"""ctypes binding of libntt.so (include/ntt.h).  Argument marshalling only:
+every step of the transform runs in the CUDA kernels behind the C ABI.
+There is no fallback -- if the library is missing, loading fails loudly."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libntt.so")
+
+NTT_OK = 0
+STATUS = {
+    0: "NTT_OK", -1: "NTT_ERR_INVALID_N", -2: "NTT_ERR_INVALID_PRIME", -3: "NTT_ERR_INVALID_ARG",
+    -4: "NTT_ERR_MISALIGNED", -5: "NTT_ERR_WRONG_DEVICE", -6: "NTT_ERR_CUDA", -7: "NTT_ERR_OOM",
+    -8: "NTT_ERR_RANGE_EXHAUSTED",
+}
+NTT_DIR_FORWARD = 1
+NTT_DIR_INVERSE = 2
+
+# every symbol include/ntt.h declares
+EXPORTS = [
+    "ntt_find_primes", "ntt_find_psi", "ntt_plan_create", "ntt_plan_create_ex", "ntt_plan_psi",
+    "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_launch_pass", "ntt_execute_host", "ntt_workspace_words",
+    "ntt_plan_destroy", "ntt_status_string",
+]
+
+
+class NttError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        name = STATUS.get(status, str(status))
+        msg = lib().ntt_status_string(status).decode()
+        super().__init__(f"{what}: {name} ({msg})" if what else f"{name} ({msg})")
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("ot_enable", ctypes.c_int), ("ot_base", ctypes.c_uint),
+                ("ot_stages", ctypes.c_uint), ("log_n1", ctypes.c_uint)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2012_01968_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        u32, i32, u64, vp = ctypes.c_uint, ctypes.c_int, ctypes.c_uint64, ctypes.c_void_p
+        p64 = ctypes.POINTER(ctypes.c_uint64)
+        pp = ctypes.POINTER(ctypes.c_void_p)
+        L.ntt_find_primes.argtypes = [u32, u32, p64]
+        L.ntt_find_psi.argtypes = [u64, u32, p64]
+        L.ntt_plan_create.argtypes = [pp, u32, p64, u32]
+        L.ntt_plan_create_ex.argtypes = [pp, u32, p64, u32, ctypes.POINTER(Opts)]
+        L.ntt_plan_psi.argtypes = [vp, p64]
+        L.ntt_plan_info.argtypes = [vp, ctypes.POINTER(u32), ctypes.POINTER(u32), ctypes.POINTER(u32),
+                                    ctypes.POINTER(i32), ctypes.POINTER(u32), ctypes.POINTER(u32), p64]
+        L.ntt_forward.argtypes = [vp, vp, u32, vp]
+        L.ntt_inverse.argtypes = [vp, vp, u32, vp]
+        L.ntt_launch_pass.argtypes = [vp, vp, u32, u32, u32, vp]
+        L.ntt_execute_host.argtypes = [vp, u32, vp, vp, u32, vp, u64, u32]
+        L.ntt_workspace_words.argtypes = [vp, u32, u32]
+        L.ntt_workspace_words.restype = u64
+        L.ntt_plan_destroy.argtypes = [vp]
+        L.ntt_status_string.argtypes = [i32]
+        L.ntt_status_string.restype = ctypes.c_char_p
+        for name in ["ntt_find_primes", "ntt_find_psi", "ntt_plan_create", "ntt_plan_create_ex",
+                     "ntt_plan_psi", "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_launch_pass", "ntt_execute_host",
+                     "ntt_plan_destroy"]:
+            getattr(L, name).restype = i32
+        _lib = L
+    return _lib
+
+
+def check(status: int, what: str = "") -> None:
+    if status != NTT_OK:
+        raise NttError(status, what)

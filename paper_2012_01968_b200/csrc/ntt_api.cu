@@ -1,0 +1,416 @@
+// ntt_api.cu -- the C ABI of include/ntt.h: plan lifecycle, argument checks,
+// kernel dispatch and the pipelined host-buffer executor.
+#include "../../include/ntt.h"
+#include "ntt_launch.h"
+#include "params.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <thread>
+#include <vector>
+
+using ntt::KArgs;
+using ntt::PrimeConst;
+using ntt::Tw;
+
+struct ntt_plan_s {
+    int device = 0;
+    unsigned logn = 0, L = 0, log_n1 = 0;  // log_n1 == 0: single kernel per row
+    int ot_enable = 0;
+    unsigned ot_base = 0, ot_logb = 0, ot_stages = 0;
+    std::vector<uint64_t> primes, psis;
+    Tw* d_fwd = nullptr;  // [L][N]
+    Tw* d_inv = nullptr;  // [L][N]
+    Tw* d_ot_fwd = nullptr;  // [L][B + N/B]
+    Tw* d_ot_inv = nullptr;
+    PrimeConst* d_pc = nullptr;  // [L]
+    uint64_t table_bytes = 0;
+};
+
+namespace {
+
+unsigned ilog2(uint64_t v)
+{
+    unsigned l = 0;
+    while ((1ull << l) < v) ++l;
+    return l;
+}
+
+bool pow2_in(unsigned n, unsigned lo_log, unsigned hi_log)
+{
+    return n && (n & (n - 1)) == 0 && ilog2(n) >= lo_log && ilog2(n) <= hi_log;
+}
+
+// Two-kernel split: N1 = 2^log_n1 column transforms, N2 contiguous.
+// Rows up to 2^13 words (64 KiB) are handled by one kernel in SMEM.
+unsigned default_log_n1(unsigned logn)
+{
+    switch (logn) {
+        case 14: return 7;
+        case 15: return 7;
+        case 16: return 8;
+        case 17: return 8;
+        default: return 0;
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard()
+    {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+void free_plan_memory(ntt_plan_s* p)
+{
+    cudaFree(p->d_fwd);
+    cudaFree(p->d_inv);
+    cudaFree(p->d_ot_fwd);
+    cudaFree(p->d_ot_inv);
+    cudaFree(p->d_pc);
+    p->d_fwd = p->d_inv = p->d_ot_fwd = p->d_ot_inv = nullptr;
+    p->d_pc = nullptr;
+}
+
+ntt_status_t check_data(const ntt_plan_s* plan, const void* data)
+{
+    if (!plan || !data) return NTT_ERR_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(data) & 15u) return NTT_ERR_MISALIGNED;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, data) != cudaSuccess) {
+        cudaGetLastError();
+        return NTT_ERR_WRONG_DEVICE;
+    }
+    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) return NTT_ERR_WRONG_DEVICE;
+    if (at.device != plan->device) return NTT_ERR_WRONG_DEVICE;
+    return NTT_OK;
+}
+
+KArgs base_args(const ntt_plan_s* plan, uint64_t* data, unsigned batch, bool inverse)
+{
+    KArgs a{};
+    a.data = data;
+    a.tab = inverse ? plan->d_inv : plan->d_fwd;
+    a.ot = inverse ? plan->d_ot_inv : plan->d_ot_fwd;
+    a.pc = plan->d_pc;
+    a.L = plan->L;
+    a.batch = batch;
+    a.logn = plan->logn;
+    a.log_n1 = plan->log_n1;
+    a.ot_logb = plan->ot_logb;
+    a.iters = 1;
+    return a;
+}
+
+// Enqueue one direction (pass < 0: all passes) on `st`; no checks.
+cudaError_t enqueue(const ntt_plan_s* plan, uint64_t* data, unsigned batch, bool inverse, cudaStream_t st,
+                    int pass = -1)
+{
+    KArgs a = base_args(plan, data, batch, inverse);
+    const uint32_t rows = batch * plan->L;
+    const int ots = plan->ot_enable ? (int)plan->ot_stages : 0;
+    if (plan->log_n1 == 0) {
+        a.total_blocks = rows;
+        return ntt::launch_single(inverse, a, ots, 1, st);
+    }
+    a.total_blocks = rows << plan->log_n1;
+    a.log_tiles = plan->logn - plan->log_n1 - 4;
+    cudaError_t e = cudaSuccess;
+    if (!inverse) {
+        if (pass != 1 && (e = ntt::launch_k1(false, a, rows, st)) != cudaSuccess) return e;
+        if (pass != 0) e = ntt::launch_k2(false, a, ots, 1, st);
+        return e;
+    }
+    if (pass != 1 && (e = ntt::launch_k2(true, a, ots, 1, st)) != cudaSuccess) return e;
+    if (pass != 0) e = ntt::launch_k1(true, a, rows, st);
+    return e;
+}
+
+ntt_status_t run(ntt_plan_t plan, uint64_t* data, unsigned batch, void* stream, bool inverse, int pass = -1)
+{
+    if (!plan || !data) return NTT_ERR_INVALID_ARG;
+    if (batch == 0) return NTT_OK;
+    ntt_status_t s = check_data(plan, data);
+    if (s != NTT_OK) return s;
+    if ((uint64_t)batch * plan->L * ((uint64_t)1 << plan->log_n1) >= (1ull << 31)) return NTT_ERR_INVALID_ARG;
+    DeviceGuard g(plan->device);
+    return enqueue(plan, data, batch, inverse, (cudaStream_t)stream, pass) == cudaSuccess ? NTT_OK : NTT_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ntt_status_string(ntt_status_t s)
+{
+    switch (s) {
+        case NTT_OK: return "ok";
+        case NTT_ERR_INVALID_N: return "N must be a power of two in [2, 2^17]";
+        case NTT_ERR_INVALID_PRIME: return "prime must be prime, = 1 mod 2N, < 2^60 and distinct";
+        case NTT_ERR_INVALID_ARG: return "invalid argument";
+        case NTT_ERR_MISALIGNED: return "data pointer must be 16-byte aligned";
+        case NTT_ERR_WRONG_DEVICE: return "data pointer is not device memory of the plan's device";
+        case NTT_ERR_CUDA: return "CUDA error";
+        case NTT_ERR_OOM: return "out of memory";
+        case NTT_ERR_RANGE_EXHAUSTED: return "not enough NTT primes in [2^59, 2^60)";
+    }
+    return "unknown status";
+}
+
+ntt_status_t ntt_find_primes(unsigned n, unsigned count, uint64_t* out)
+{
+    if (!pow2_in(n, 1, 17)) return NTT_ERR_INVALID_N;
+    if (!out || count == 0) return NTT_ERR_INVALID_ARG;
+    std::vector<uint64_t> v;
+    if (!nttp::ntt_primes(n, count, v)) return NTT_ERR_RANGE_EXHAUSTED;
+    std::copy(v.begin(), v.end(), out);
+    return NTT_OK;
+}
+
+ntt_status_t ntt_find_psi(uint64_t p, unsigned n, uint64_t* psi)
+{
+    if (!pow2_in(n, 1, 17)) return NTT_ERR_INVALID_N;
+    if (!psi) return NTT_ERR_INVALID_ARG;
+    const uint64_t r = nttp::smallest_psi(p, n);
+    if (!r) return NTT_ERR_INVALID_PRIME;
+    *psi = r;
+    return NTT_OK;
+}
+
+ntt_status_t ntt_plan_create(ntt_plan_t* plan, unsigned n, const uint64_t* primes, unsigned L)
+{
+    return ntt_plan_create_ex(plan, n, primes, L, nullptr);
+}
+
+ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* primes, unsigned L, const ntt_opts_t* o)
+{
+    if (!out) return NTT_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (!primes || L == 0) return NTT_ERR_INVALID_ARG;
+    if (!pow2_in(n, 1, 17)) return NTT_ERR_INVALID_N;
+    ntt_opts_t opts{};
+    if (o) opts = *o;
+    const unsigned logn = ilog2(n);
+
+    std::vector<uint64_t> pr(primes, primes + L);
+    for (unsigned i = 0; i < L; ++i) {
+        if (!nttp::valid_ntt_prime(pr[i], n)) return NTT_ERR_INVALID_PRIME;
+        for (unsigned j = 0; j < i; ++j)
+            if (pr[j] == pr[i]) return NTT_ERR_INVALID_PRIME;
+    }
+
+    // options
+    unsigned log_n1 = default_log_n1(logn);
+    if (opts.log_n1) {
+        if (logn <= 13) {
+            log_n1 = 0;  // one kernel holds the row
+        } else {
+            const unsigned l1 = opts.log_n1, l2 = logn - opts.log_n1;
+            if (l1 < 6 || l1 > 10 || l2 < 6 || l2 > 11) return NTT_ERR_INVALID_ARG;
+            log_n1 = l1;
+        }
+    }
+    if (opts.ot_enable < -1 || opts.ot_enable > 1) return NTT_ERR_INVALID_ARG;
+    const int ot_enable = opts.ot_enable == 1;
+    unsigned ot_base = opts.ot_base;
+    if (ot_base == 0) ot_base = logn >= 11 ? 1024u : (1u << ((logn + 1) / 2));
+    if ((ot_base & (ot_base - 1)) || ot_base > n) return NTT_ERR_INVALID_ARG;
+    unsigned ot_stages = opts.ot_stages ? opts.ot_stages : 2;
+    if (ot_stages > 2) return NTT_ERR_INVALID_ARG;
+    const unsigned last_kernel_stages = log_n1 ? logn - log_n1 : logn;
+    if (ot_stages > last_kernel_stages) ot_stages = last_kernel_stages;
+
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return NTT_ERR_CUDA;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return NTT_ERR_CUDA;
+    }
+
+    ntt_plan_s* p = new (std::nothrow) ntt_plan_s;
+    if (!p) return NTT_ERR_OOM;
+    p->device = dev;
+    p->logn = logn;
+    p->L = L;
+    p->log_n1 = log_n1;
+    p->ot_enable = ot_enable;
+    p->ot_base = ot_base;
+    p->ot_logb = ilog2(ot_base);
+    p->ot_stages = ot_stages;
+    p->primes = pr;
+    p->psis.assign(L, 0);
+
+    // host tables, one thread per hardware thread over primes
+    const uint64_t N = n, NOT = ot_base + N / ot_base;
+    std::vector<Tw> h_fwd(N * L), h_inv(N * L), h_otf(NOT * L), h_oti(NOT * L);
+    std::vector<PrimeConst> h_pc(L);
+    unsigned nth = std::max(1u, std::min(L, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nth; ++t)
+        th.emplace_back([&, t] {
+            for (unsigned l = t; l < L; l += nth) {
+                const uint64_t q = pr[l];
+                const uint64_t psi = nttp::smallest_psi(q, N);
+                const uint64_t psi_inv = nttp::pow_mod(psi, q - 2, q);
+                p->psis[l] = psi;
+                static_assert(sizeof(nttp::Twiddle) == sizeof(Tw), "layout");
+                nttp::bitrev_power_table(q, psi, logn, reinterpret_cast<nttp::Twiddle*>(&h_fwd[l * N]));
+                nttp::bitrev_power_table(q, psi_inv, logn, reinterpret_cast<nttp::Twiddle*>(&h_inv[l * N]));
+                nttp::ot_base_tables(q, psi, N, ot_base, reinterpret_cast<nttp::Twiddle*>(&h_otf[l * NOT]));
+                nttp::ot_base_tables(q, psi_inv, N, ot_base, reinterpret_cast<nttp::Twiddle*>(&h_oti[l * NOT]));
+                const uint64_t ninv = nttp::pow_mod(N % q, q - 2, q);
+                const uint64_t ninv_psi = nttp::mul_mod(ninv, h_inv[l * N + (N > 1 ? 1 : 0)].w, q);
+                PrimeConst c;
+                c.p = q;
+                c.p2 = 2 * q;
+                nttp::Twiddle t1 = nttp::shoup_pair(ninv, q), t2 = nttp::shoup_pair(ninv_psi, q);
+                c.ninv = Tw{t1.w, t1.wb};
+                c.ninv_psi = Tw{t2.w, t2.wb};
+                h_pc[l] = c;
+            }
+        });
+    for (auto& t : th) t.join();
+
+    const size_t bt = sizeof(Tw) * N * L, bo = sizeof(Tw) * NOT * L, bp = sizeof(PrimeConst) * L;
+    if (cudaMalloc(&p->d_fwd, bt) != cudaSuccess || cudaMalloc(&p->d_inv, bt) != cudaSuccess ||
+        cudaMalloc(&p->d_ot_fwd, bo) != cudaSuccess || cudaMalloc(&p->d_ot_inv, bo) != cudaSuccess ||
+        cudaMalloc(&p->d_pc, bp) != cudaSuccess) {
+        cudaGetLastError();
+        free_plan_memory(p);
+        delete p;
+        return NTT_ERR_OOM;
+    }
+    if (cudaMemcpy(p->d_fwd, h_fwd.data(), bt, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(p->d_inv, h_inv.data(), bt, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(p->d_ot_fwd, h_otf.data(), bo, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(p->d_ot_inv, h_oti.data(), bo, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(p->d_pc, h_pc.data(), bp, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaGetLastError();
+        free_plan_memory(p);
+        delete p;
+        return NTT_ERR_CUDA;
+    }
+    p->table_bytes = 2 * bt + 2 * bo + bp;
+    *out = p;
+    return NTT_OK;
+}
+
+ntt_status_t ntt_plan_psi(ntt_plan_t plan, uint64_t* psi_out)
+{
+    if (!plan || !psi_out) return NTT_ERR_INVALID_ARG;
+    std::copy(plan->psis.begin(), plan->psis.end(), psi_out);
+    return NTT_OK;
+}
+
+ntt_status_t ntt_plan_info(ntt_plan_t plan, unsigned* L, unsigned* logn, unsigned* log_n1, int* ot_enable,
+                           unsigned* ot_base, unsigned* ot_stages, uint64_t* table_bytes)
+{
+    if (!plan) return NTT_ERR_INVALID_ARG;
+    if (L) *L = plan->L;
+    if (logn) *logn = plan->logn;
+    if (log_n1) *log_n1 = plan->log_n1;
+    if (ot_enable) *ot_enable = plan->ot_enable;
+    if (ot_base) *ot_base = plan->ot_base;
+    if (ot_stages) *ot_stages = plan->ot_stages;
+    if (table_bytes) *table_bytes = plan->table_bytes;
+    return NTT_OK;
+}
+
+ntt_status_t ntt_forward(ntt_plan_t plan, uint64_t* data, unsigned batch, void* stream)
+{
+    return run(plan, data, batch, stream, false);
+}
+
+ntt_status_t ntt_inverse(ntt_plan_t plan, uint64_t* data, unsigned batch, void* stream)
+{
+    return run(plan, data, batch, stream, true);
+}
+
+ntt_status_t ntt_launch_pass(ntt_plan_t plan, uint64_t* data, unsigned batch, unsigned dir, unsigned pass,
+                             void* stream)
+{
+    if (!plan || (dir != NTT_DIR_FORWARD && dir != NTT_DIR_INVERSE)) return NTT_ERR_INVALID_ARG;
+    if (pass > 1 || (pass == 1 && plan->log_n1 == 0)) return NTT_ERR_INVALID_ARG;
+    return run(plan, data, batch, stream, dir == NTT_DIR_INVERSE, plan->log_n1 == 0 ? -1 : (int)pass);
+}
+
+static unsigned auto_chunk(const ntt_plan_s* plan, unsigned batch, unsigned chunk)
+{
+    if (chunk) return std::min(chunk, batch);
+    const uint64_t ct_bytes = (uint64_t)plan->L * 8ull << plan->logn;
+    uint64_t c = std::max<uint64_t>(1, (128ull << 20) / ct_bytes);  // ~128 MiB per pipeline step
+    return (unsigned)std::min<uint64_t>(c, batch);
+}
+
+uint64_t ntt_workspace_words(ntt_plan_t plan, unsigned batch, unsigned chunk)
+{
+    if (!plan || batch == 0) return 0;
+    const unsigned c = auto_chunk(plan, batch, chunk);
+    const unsigned nbuf = c < batch ? 2 : 1;
+    return (uint64_t)nbuf * c * plan->L << plan->logn;
+}
+
+ntt_status_t ntt_execute_host(ntt_plan_t plan, unsigned flags, const uint64_t* host_in, uint64_t* host_out,
+                              unsigned batch, uint64_t* workspace, uint64_t workspace_words, unsigned chunk)
+{
+    if (!plan || !host_in || !host_out || (flags & ~3u)) return NTT_ERR_INVALID_ARG;
+    if (batch == 0) return NTT_OK;
+    ntt_status_t s = check_data(plan, workspace);
+    if (s != NTT_OK) return s;
+    const unsigned c = auto_chunk(plan, batch, chunk);
+    if (workspace_words < ntt_workspace_words(plan, batch, c)) return NTT_ERR_INVALID_ARG;
+    DeviceGuard g(plan->device);
+    const uint64_t ct_words = (uint64_t)plan->L << plan->logn;
+    cudaStream_t st[2];
+    if (cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking) != cudaSuccess) return NTT_ERR_CUDA;
+    if (cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking) != cudaSuccess) {
+        cudaStreamDestroy(st[0]);
+        return NTT_ERR_CUDA;
+    }
+    cudaError_t e = cudaSuccess;
+    unsigned k = 0;
+    for (unsigned b0 = 0; b0 < batch && e == cudaSuccess; b0 += c, ++k) {
+        const unsigned nb = std::min(c, batch - b0);
+        cudaStream_t sk = st[k & 1];
+        uint64_t* buf = workspace + (uint64_t)(k & 1) * c * ct_words;
+        const size_t bytes = (size_t)nb * ct_words * 8;
+        e = cudaMemcpyAsync(buf, host_in + (uint64_t)b0 * ct_words, bytes, cudaMemcpyHostToDevice, sk);
+        if (e == cudaSuccess && (flags & NTT_DIR_FORWARD)) e = enqueue(plan, buf, nb, false, sk);
+        if (e == cudaSuccess && (flags & NTT_DIR_INVERSE)) e = enqueue(plan, buf, nb, true, sk);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(host_out + (uint64_t)b0 * ct_words, buf, bytes, cudaMemcpyDeviceToHost, sk);
+    }
+    cudaError_t e0 = cudaStreamSynchronize(st[0]), e1 = cudaStreamSynchronize(st[1]);
+    cudaStreamDestroy(st[0]);
+    cudaStreamDestroy(st[1]);
+    if (e == cudaSuccess) e = e0 != cudaSuccess ? e0 : e1;
+    return e == cudaSuccess ? NTT_OK : NTT_ERR_CUDA;
+}
+
+ntt_status_t ntt_plan_destroy(ntt_plan_t plan)
+{
+    if (!plan) return NTT_OK;
+    {
+        DeviceGuard g(plan->device);
+        free_plan_memory(plan);
+    }
+    delete plan;
+    return NTT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,313 @@
+// ntt_kernels.cu -- the sm_100a kernels of the batched negacyclic NTT / iNTT.
+//
+//   k_cols   : Kernel-1 (forward) / Kernel-1' (inverse) of the two-kernel
+//              split N = N1 * N2: the N1-point column transforms
+//              over stride-N2 columns, a 16-column tile per CTA so every global
+//              access is a full 128-byte row segment (coalescing),
+//              twiddles Psi[1..N1) preloaded into SMEM.
+//   k_contig : Kernel-2 / Kernel-2' -- contiguous N2-point blocks -- and the
+//              single-kernel path for N <= 2^13, where one CTA holds whole rows.
+//              Optional on-the-fly twiddling on the last (forward)
+//              or first (inverse) 1-2 stages.
+//
+// Both run per-thread radix-16 register NTTs with SMEM exchanges between
+// rounds; 64-bit words, Shoup modmul.
+#include "ntt_device.cuh"
+#include "ntt_launch.h"
+
+#include <atomic>
+
+namespace ntt {
+
+// ---------------------------------------------------------------- Kernel-1
+template <int LOGN1, bool INV>
+__global__ void __launch_bounds__(1 << LOGN1) k_cols(const KArgs a)
+{
+    using SC = Sched<LOGN1>;
+    static_assert(SC::E == 16, "column kernel needs N1 >= 16");
+    constexpr int M = SC::M, NR = SC::NR;
+    extern __shared__ __align__(16) uint64_t sm[];  // [M][16] words, then Tw[M]
+    Tw* tws = reinterpret_cast<Tw*>(sm + M * 16);
+
+    const uint32_t tid = threadIdx.x, c = tid & 15u, tib = tid >> 4;
+    const uint32_t tile = blockIdx.x & ((1u << a.log_tiles) - 1u);
+    const uint32_t q = blockIdx.x >> a.log_tiles;  // prime-major: q = l * batch + b
+    const uint32_t l = q / a.batch, b = q - l * a.batch;
+    const uint32_t logn2 = a.logn - LOGN1;
+    uint64_t* col = a.data + (((uint64_t)b * a.L + l) << a.logn) + tile * 16u + c;
+    const Tw* tab = a.tab + ((uint64_t)l << a.logn);
+    const PrimeConst pc = a.pc[l];
+
+    tws[tid] = ldg_tw(tab + tid);  // Psi[0..N1): the first log N1 stages' table
+    __syncthreads();
+    auto tabf = [&](uint32_t idx) { return tws[idx]; };
+    auto otf = [&](uint32_t) { return TwMul<true>{}; };  // OT never reaches Kernel-1
+
+    uint64_t x[16];
+    auto g_load = [&](auto ri) {
+        using Geo = RoundGeo<LOGN1, decltype(ri)::value>;
+#pragma unroll
+        for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+            for (int k = 0; k < Geo::R; ++k)
+                x[qd * Geo::R + k] = col[(uint64_t)Geo::elem(qd * SC::TB + tib, k) << logn2];
+    };
+    auto g_store = [&](auto ri) {
+        using Geo = RoundGeo<LOGN1, decltype(ri)::value>;
+#pragma unroll
+        for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+            for (int k = 0; k < Geo::R; ++k)
+                col[(uint64_t)Geo::elem(qd * SC::TB + tib, k) << logn2] = x[qd * Geo::R + k];
+    };
+    auto s_load = [&](auto ri) {
+        using Geo = RoundGeo<LOGN1, decltype(ri)::value>;
+#pragma unroll
+        for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+            for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = sm[Geo::elem(qd * SC::TB + tib, k) * 16 + c];
+    };
+    auto s_store = [&](auto ri) {
+        using Geo = RoundGeo<LOGN1, decltype(ri)::value>;
+#pragma unroll
+        for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+            for (int k = 0; k < Geo::R; ++k) sm[Geo::elem(qd * SC::TB + tib, k) * 16 + c] = x[qd * Geo::R + k];
+    };
+
+    if constexpr (!INV) {
+        static_for<NR>([&](auto ri) {
+            constexpr int RI = decltype(ri)::value;
+            if constexpr (RI == 0) {
+                g_load(ri);
+            } else {
+                s_load(ri);
+            }
+            ct_round<LOGN1, RI, 1 << 20>(x, tib, 1u, tabf, otf, pc.p, pc.p2);
+            if constexpr (RI == NR - 1) {
+                g_store(ri);
+            } else {
+                s_store(ri);
+                __syncthreads();
+            }
+        });
+    } else {
+        static_for<NR>([&](auto rj) {
+            constexpr int RI = NR - 1 - decltype(rj)::value;
+            using RC = std::integral_constant<int, RI>;
+            if constexpr (RI == NR - 1) {
+                g_load(RC{});
+            } else {
+                s_load(RC{});
+            }
+            gs_round<LOGN1, RI, 1 << 20, true>(x, tib, 1u, tabf, otf, pc.p, pc.p2, pc);
+            if constexpr (RI == 0) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) x[k] = csub(x[k], pc.p);  // canonical [0, p)
+                g_store(RC{});
+            } else {
+                s_store(RC{});
+                __syncthreads();
+            }
+        });
+    }
+}
+
+// ---------------------------------------------------------------- contiguous
+template <int LOGM>
+struct ContigCfg {
+    static constexpr int TB = Sched<LOGM>::TB;
+    static constexpr int CT = TB > 256 ? TB : 256;  // threads per CTA
+    static constexpr int NB = CT / TB;              // blocks per CTA iteration
+    static constexpr size_t SMEM = (size_t)NB * (1 << LOGM) * 8;
+};
+
+template <int LOGM, bool INV, bool FUSE0, int OTS>
+__global__ void __launch_bounds__(ContigCfg<LOGM>::CT) k_contig(const KArgs a)
+{
+    using SC = Sched<LOGM>;
+    using CC = ContigCfg<LOGM>;
+    constexpr int M = SC::M, E = SC::E, TB = SC::TB, NR = SC::NR;
+    constexpr int OT_FROM = OTS ? LOGM - OTS : (1 << 20);
+    extern __shared__ __align__(16) uint64_t sm[];
+
+    const uint32_t tid = threadIdx.x, blk = tid / TB, tib = tid % TB;
+    uint64_t* sb = sm + blk * M;
+    const uint32_t n1mask = (1u << a.log_n1) - 1u;
+    const uint32_t B_ot = 1u << a.ot_logb;
+
+    for (uint32_t it = 0; it < a.iters; ++it) {
+        uint32_t gb = (blockIdx.x * a.iters + it) * CC::NB + blk;
+        const bool active = gb < a.total_blocks;
+        if (!active) gb = a.total_blocks - 1;  // compute a valid block, skip its store
+        const uint32_t bb = gb & n1mask, q = gb >> a.log_n1;
+        const uint32_t l = q / a.batch, b = q - l * a.batch;
+        uint64_t* g = a.data + (((uint64_t)b * a.L + l) << a.logn) + (uint64_t)bb * M;
+        const uint32_t F = (1u << a.log_n1) + bb;
+        const Tw* tab = a.tab + ((uint64_t)l << a.logn);
+        const Tw* ot = a.ot + (uint64_t)l * (B_ot + ((1u << a.logn) >> a.ot_logb));
+        const PrimeConst pc = a.pc[l];
+        auto tabf = [&](uint32_t idx) { return ldg_tw(tab + idx); };
+        auto otf = [&](uint32_t idx) {
+            // exponent of Psi[idx] is bitrev_logn(idx) = e = q*B + r
+            const uint32_t e = __brev(idx) >> (32 - a.logn);
+            return TwMul<true>{ldg_tw(ot + (e & (B_ot - 1u))), ldg_tw(ot + B_ot + (e >> a.ot_logb))};
+        };
+
+        // global -> SMEM, 16-byte vectors, coalesced
+#pragma unroll
+        for (int j = 0; j < E / 2; ++j) {
+            const uint32_t ch = j * TB + tib;
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(g + 2 * ch);
+            *reinterpret_cast<ulonglong2*>(sb + swz(2 * ch)) = v;
+        }
+        __syncthreads();
+
+        uint64_t x[16];
+        auto s_load = [&](auto ri) {
+            using Geo = RoundGeo<LOGM, decltype(ri)::value>;
+#pragma unroll
+            for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+                for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = sb[swz(Geo::elem(qd * TB + tib, k))];
+        };
+        auto s_store = [&](auto ri) {
+            using Geo = RoundGeo<LOGM, decltype(ri)::value>;
+#pragma unroll
+            for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+                for (int k = 0; k < Geo::R; ++k) sb[swz(Geo::elem(qd * TB + tib, k))] = x[qd * Geo::R + k];
+        };
+
+        if constexpr (!INV) {
+            static_for<NR>([&](auto ri) {
+                constexpr int RI = decltype(ri)::value;
+                s_load(ri);
+                ct_round<LOGM, RI, OT_FROM>(x, tib, F, tabf, otf, pc.p, pc.p2);
+                if constexpr (RI == NR - 1) {
+#pragma unroll
+                    for (int k = 0; k < E; ++k) x[k] = csub(csub(x[k], pc.p2), pc.p);  // [0,4p) -> [0,p)
+                }
+                s_store(ri);
+                __syncthreads();
+            });
+        } else {
+            static_for<NR>([&](auto rj) {
+                constexpr int RI = NR - 1 - decltype(rj)::value;
+                using RC = std::integral_constant<int, RI>;
+                s_load(RC{});
+                gs_round<LOGM, RI, OT_FROM, FUSE0>(x, tib, F, tabf, otf, pc.p, pc.p2, pc);
+                if constexpr (FUSE0 && RI == 0) {
+#pragma unroll
+                    for (int k = 0; k < E; ++k) x[k] = csub(x[k], pc.p);
+                }
+                s_store(RC{});
+                __syncthreads();
+            });
+        }
+
+        // SMEM -> global
+        if (active) {
+#pragma unroll
+            for (int j = 0; j < E / 2; ++j) {
+                const uint32_t ch = j * TB + tib;
+                *reinterpret_cast<ulonglong2*>(g + 2 * ch) = *reinterpret_cast<const ulonglong2*>(sb + swz(2 * ch));
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- dispatch
+namespace {
+
+// true if this device already had the attribute set; marks it otherwise
+bool set_once(std::atomic<uint64_t>& mask)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    return mask.fetch_or(bit) & bit;
+}
+
+template <int LOGN1, bool INV>
+cudaError_t launch_cols_t(const KArgs& a, uint32_t rows, cudaStream_t st)
+{
+    constexpr int M = 1 << LOGN1;
+    const size_t smem = (size_t)M * 16 * 8 + (size_t)M * sizeof(Tw);
+    auto fn = k_cols<LOGN1, INV>;
+    static std::atomic<uint64_t> attr_set{0};  // one bit per device
+    if (!set_once(attr_set)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const uint64_t grid = (uint64_t)rows << a.log_tiles;
+    fn<<<(unsigned)grid, M, smem, st>>>(a);
+    return cudaPeekAtLastError();
+}
+
+template <int LOGM, bool INV, bool FUSE0, int OTS>
+cudaError_t launch_contig_t(KArgs a, uint32_t iters, cudaStream_t st)
+{
+    using CC = ContigCfg<LOGM>;
+    auto fn = k_contig<LOGM, INV, FUSE0, OTS>;
+    static std::atomic<uint64_t> attr_set{0};  // one bit per device
+    if (!set_once(attr_set)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
+    a.iters = iters;
+    const uint64_t per_cta = (uint64_t)CC::NB * iters;
+    const uint64_t grid = (a.total_blocks + per_cta - 1) / per_cta;
+    fn<<<(unsigned)grid, CC::CT, CC::SMEM, st>>>(a);
+    return cudaPeekAtLastError();
+}
+
+template <int LOGM, bool INV, bool FUSE0>
+cudaError_t launch_contig_ot(const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
+{
+    switch (ots) {
+        case 0: return launch_contig_t<LOGM, INV, FUSE0, 0>(a, iters, st);
+        case 1: return launch_contig_t<LOGM, INV, FUSE0, (LOGM >= 1 ? 1 : 0)>(a, iters, st);
+        default: return launch_contig_t<LOGM, INV, FUSE0, (LOGM >= 2 ? 2 : LOGM)>(a, iters, st);
+    }
+}
+
+template <bool INV, bool FUSE0, int... Ls>
+cudaError_t contig_switch(int logm, const KArgs& a, int ots, uint32_t iters, cudaStream_t st,
+                          std::integer_sequence<int, Ls...>)
+{
+    cudaError_t err = cudaErrorInvalidValue;
+    ((logm == Ls ? (err = launch_contig_ot<Ls, INV, FUSE0>(a, ots, iters, st), 0) : 0), ...);
+    return err;
+}
+
+template <bool INV, int... Ls>
+cudaError_t cols_switch(int logn1, const KArgs& a, uint32_t rows, cudaStream_t st, std::integer_sequence<int, Ls...>)
+{
+    cudaError_t err = cudaErrorInvalidValue;
+    ((logn1 == Ls ? (err = launch_cols_t<Ls, INV>(a, rows, st), 0) : 0), ...);
+    return err;
+}
+
+}  // namespace
+
+// Supported sizes: single kernel LOGM 1..13; Kernel-2 LOGM 6..11; Kernel-1 LOGN1 6..10.
+using SingleSizes = std::integer_sequence<int, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13>;
+using K2Sizes = std::integer_sequence<int, 6, 7, 8, 9, 10, 11>;
+using K1Sizes = std::integer_sequence<int, 6, 7, 8, 9, 10>;
+
+cudaError_t launch_single(bool inverse, const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
+{
+    return inverse ? contig_switch<true, true>((int)a.logn, a, ots, iters, st, SingleSizes{})
+                   : contig_switch<false, false>((int)a.logn, a, ots, iters, st, SingleSizes{});
+}
+
+cudaError_t launch_k2(bool inverse, const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
+{
+    const int logm = (int)(a.logn - a.log_n1);
+    return inverse ? contig_switch<true, false>(logm, a, ots, iters, st, K2Sizes{})
+                   : contig_switch<false, false>(logm, a, ots, iters, st, K2Sizes{});
+}
+
+cudaError_t launch_k1(bool inverse, const KArgs& a, uint32_t rows, cudaStream_t st)
+{
+    return inverse ? cols_switch<true>((int)a.log_n1, a, rows, st, K1Sizes{})
+                   : cols_switch<false>((int)a.log_n1, a, rows, st, K1Sizes{});
+}
+
+}  // namespace ntt

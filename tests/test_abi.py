@@ -1,0 +1,120 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol the
+header declares, and its host-only logic (prime scan, psi, argument checks)
+behaves; no compute call needs a GPU here."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import oracle
+from paper_2012_01968_b200 import _native
+from paper_2012_01968_b200 import find_primes, find_psi, NttError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "ntt.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ntt_[a-z_]+)\s*\(", src)))
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    lib = _native.lib()
+    declared = header_functions()
+    assert declared, "no declarations parsed"
+    assert sorted(declared) == sorted(_native.EXPORTS)
+    for name in declared:
+        assert hasattr(lib, name), name
+    # exported with C linkage (no C++ mangling)
+    out = os.popen(f"nm -D --defined-only {_native.LIB_PATH}").read()
+    for name in declared:
+        assert re.search(rf"\bT {name}$", out, re.M), name
+
+
+def test_library_is_sm100a():
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {_native.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+
+
+def test_status_strings():
+    lib = _native.lib()
+    for code in range(-8, 1):
+        assert lib.ntt_status_string(code)
+
+
+@pytest.mark.parametrize("logn,count", [(1, 3), (12, 4), (15, 15), (16, 45), (17, 60)])
+def test_host_primes_match_oracle(logn, count):
+    N = 1 << logn
+    assert find_primes(N, count) == oracle.find_primes(N, count)
+
+
+@pytest.mark.parametrize("logn", [1, 4, 12, 15, 16, 17])
+def test_host_psi_matches_oracle(logn):
+    N = 1 << logn
+    for p in oracle.find_primes(N, 3):
+        assert find_psi(p, N) == oracle.find_psi(p, N)
+
+
+def test_host_helper_errors():
+    with pytest.raises(NttError) as e:
+        find_primes(3, 1)
+    assert e.value.status == -1
+    with pytest.raises(NttError) as e:
+        find_primes(1 << 18, 1)
+    assert e.value.status == -1
+    with pytest.raises(NttError) as e:
+        find_psi(19, 4)
+    assert e.value.status == -2
+    out = (ctypes.c_uint64 * 1)()
+    assert _native.lib().ntt_find_primes(8, 0, out) == -3
+
+
+def test_plan_create_argument_errors_before_device():
+    lib = _native.lib()
+    h = ctypes.c_void_p()
+    p = oracle.find_primes(1 << 12, 2)
+    arr = (ctypes.c_uint64 * 2)(*p)
+    assert lib.ntt_plan_create(ctypes.byref(h), 3000, arr, 2) == -1          # N not a power of two
+    assert lib.ntt_plan_create(ctypes.byref(h), 1 << 18, arr, 2) == -1       # N too large
+    assert lib.ntt_plan_create(ctypes.byref(h), 1 << 12, None, 2) == -3      # no primes
+    assert lib.ntt_plan_create(ctypes.byref(h), 1 << 12, arr, 0) == -3       # L = 0
+    bad = (ctypes.c_uint64 * 2)(p[0], p[0])
+    assert lib.ntt_plan_create(ctypes.byref(h), 1 << 12, bad, 2) == -2       # repeated prime
+    bad = (ctypes.c_uint64 * 1)(p[0] + 2 * (1 << 12))                        # = 1 mod 2N, composite?
+    if not oracle.is_prime(bad[0]):
+        assert lib.ntt_plan_create(ctypes.byref(h), 1 << 12, bad, 1) == -2
+    big = oracle.find_primes(1 << 12, 1, 1 << 60, 1 << 61)                 # >= 2^60: lazy headroom gone
+    bad = (ctypes.c_uint64 * 1)(big[0])
+    assert lib.ntt_plan_create(ctypes.byref(h), 1 << 12, bad, 1) == -2
+    bad = (ctypes.c_uint64 * 1)(17)                                          # 17 != 1 mod 2^13
+    assert lib.ntt_plan_create(ctypes.byref(h), 1 << 12, bad, 1) == -2
+    assert lib.ntt_forward(None, None, 1, None) == -3
+    assert lib.ntt_inverse(None, None, 1, None) == -3
+    assert lib.ntt_plan_destroy(None) == 0
+
+
+def test_no_cpu_fallback_without_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    lib = _native.lib()
+    h = ctypes.c_void_p()
+    p = oracle.find_primes(1 << 12, 1)
+    arr = (ctypes.c_uint64 * 1)(*p)
+    assert lib.ntt_plan_create(ctypes.byref(h), 1 << 12, arr, 1) == -6      # NTT_ERR_CUDA, loudly
+
+
+def test_product_package_does_not_touch_oracle():
+    """The product path never imports, links, includes or reads the oracle."""
+    pkg = os.path.join(ROOT, "paper_2012_01968_b200")
+    pat = re.compile(r"^\s*(import\s+oracle|from\s+oracle\b)|#include\s*[<\"].*oracle|liboracle|ntt_oracle",
+                     re.M)
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not pat.search(src), f
+    out = os.popen(f"nm -D {_native.LIB_PATH}").read()
+    assert "oracle_" not in out
