@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <thread>
@@ -28,6 +30,7 @@ struct ntt_plan_s {
     Tw* d_ot_inv = nullptr;
     PrimeConst* d_pc = nullptr;  // [L]
     uint64_t table_bytes = 0;
+    int loge_k1 = 4, loge_k2 = 4;  // per-thread radix of Kernel-1 / Kernel-2
 };
 
 namespace {
@@ -128,12 +131,12 @@ cudaError_t enqueue(const ntt_plan_s* plan, uint64_t* data, unsigned batch, bool
     a.log_tiles = plan->logn - plan->log_n1 - 4;
     cudaError_t e = cudaSuccess;
     if (!inverse) {
-        if (pass != 1 && (e = ntt::launch_k1(false, a, rows, st)) != cudaSuccess) return e;
-        if (pass != 0) e = ntt::launch_k2(false, a, ots, 1, st);
+        if (pass != 1 && (e = ntt::launch_k1(false, plan->loge_k1, a, rows, st)) != cudaSuccess) return e;
+        if (pass != 0) e = ntt::launch_k2(false, plan->loge_k2, a, ots, 1, st);
         return e;
     }
-    if (pass != 1 && (e = ntt::launch_k2(true, a, ots, 1, st)) != cudaSuccess) return e;
-    if (pass != 0) e = ntt::launch_k1(true, a, rows, st);
+    if (pass != 1 && (e = ntt::launch_k2(true, plan->loge_k2, a, ots, 1, st)) != cudaSuccess) return e;
+    if (pass != 0) e = ntt::launch_k1(true, plan->loge_k1, a, rows, st);
     return e;
 }
 
@@ -254,6 +257,14 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
     p->ot_stages = ot_stages;
     p->primes = pr;
     p->psis.assign(L, 0);
+    // tuning knob (experiments only): NTT_LOGE="k1,k2" per-thread radix exponents
+    if (const char* v = std::getenv("NTT_LOGE")) {
+        int a1 = 4, a2 = 4;
+        if (std::sscanf(v, "%d,%d", &a1, &a2) == 2 && (a1 == 3 || a1 == 4) && (a2 == 3 || a2 == 4)) {
+            p->loge_k1 = a1;
+            p->loge_k2 = a2;
+        }
+    }
 
     // host tables, one thread per hardware thread over primes
     const uint64_t N = n, NOT = ot_base + N / ot_base;
@@ -278,6 +289,8 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
                 PrimeConst c;
                 c.p = q;
                 c.p2 = 2 * q;
+                c.p4 = 4 * q;
+                c.np = 0 - q;
                 nttp::Twiddle t1 = nttp::shoup_pair(ninv, q), t2 = nttp::shoup_pair(ninv_psi, q);
                 c.ninv = Tw{t1.w, t1.wb};
                 c.ninv_psi = Tw{t2.w, t2.wb};

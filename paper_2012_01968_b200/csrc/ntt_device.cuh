@@ -5,8 +5,8 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
-#include <utility>
 #include <type_traits>
+#include <utility>
 
 namespace ntt {
 
@@ -18,9 +18,10 @@ struct __align__(16) Tw {
 
 // Per-prime constants, 64 bytes.
 struct __align__(16) PrimeConst {
-    uint64_t p, p2;  // p, 2p
-    Tw ninv;         // N^-1
-    Tw ninv_psi;     // N^-1 * Psi^-1[1], the fused last GS stage (R15)
+    uint64_t p, p2, p4;  // p, 2p, 4p
+    uint64_t np;         // 2^64 - p
+    Tw ninv;             // N^-1
+    Tw ninv_psi;         // N^-1 * Psi^-1[1], the fused last GS stage (R15)
 };
 
 // Kernel arguments (passed by value, lives in the constant bank).
@@ -38,13 +39,46 @@ struct KArgs {
 };
 
 // ------------------------------------------------------------ arithmetic
-// Shoup's modmul without the final subtraction (Algorithm 4 with the lazy
-// output of R8): for any b < 2^64 and w < p < 2^62, returns r = b*w mod p
-// up to one p, r in [0, 2p).  q = floor(b * w_bar / 2^64) (R7).
-__device__ __forceinline__ uint64_t shoup_lazy(uint64_t b, uint64_t w, uint64_t wb, uint64_t p)
+// Shoup's modmul (Algorithm 4) with the lazy output of R8 and a
+// truncated quotient: for any b < 2^64 and
+// w < p < 2^60, with w_bar = floor(w 2^64 / p),
+//   q' = b1 v1 + hi(b1 v0) + hi(b0 v1)        (b = b1:b0, w_bar = v1:v0)
+// drops the low partial product and its carries, so q' <= floor(b w_bar/2^64)
+// <= q' + 2 and, with Shoup's own bound, floor(b w / p) - q' in [0, 3]:
+//   r = b w - q' p = (b w mod p) + k p,  k in {0,1,2,3}  ->  r in [0, 4p).
+// r is formed mod 2^64 as b w + q' (2^64 - p): 3 IMAD.WIDE, 2 IMAD.HI and
+// 4 IMAD on the multiply pipe.  np = 2^64 - p.
+__device__ __forceinline__ uint64_t shoup_lazy(uint64_t b, uint64_t w, uint64_t wb, uint64_t np)
 {
-    const uint64_t q = __umul64hi(b, wb);
-    return b * w - q * p;
+    uint64_t r;
+    asm("{\n\t"
+        ".reg .u32 b0, b1, v0, v1, w0, w1, n0, n1, t0, t1, q0, q1, r0, r1;\n\t"
+        ".reg .u64 q, a;\n\t"
+        "mov.b64 {b0, b1}, %1;\n\t"
+        "mov.b64 {w0, w1}, %2;\n\t"
+        "mov.b64 {v0, v1}, %3;\n\t"
+        "mov.b64 {n0, n1}, %4;\n\t"
+        "mul.hi.u32 t0, b1, v0;\n\t"
+        "mul.hi.u32 t1, b0, v1;\n\t"
+        "mul.wide.u32 q, b1, v1;\n\t"
+        "mov.b64 {q0, q1}, q;\n\t"
+        "add.cc.u32 q0, q0, t0;\n\t"
+        "addc.u32 q1, q1, 0;\n\t"
+        "add.cc.u32 q0, q0, t1;\n\t"
+        "addc.u32 q1, q1, 0;\n\t"
+        "mul.wide.u32 a, b0, w0;\n\t"
+        "mov.b64 {r0, r1}, a;\n\t"
+        "mad.lo.u32 r1, b0, w1, r1;\n\t"
+        "mad.lo.u32 r1, b1, w0, r1;\n\t"
+        "mad.lo.u32 r1, q0, n1, r1;\n\t"
+        "mad.lo.u32 r1, q1, n0, r1;\n\t"
+        "mov.b64 a, {r0, r1};\n\t"
+        "mad.wide.u32 a, q0, n0, a;\n\t"
+        "mov.b64 %0, a;\n\t"
+        "}"
+        : "=l"(r)
+        : "l"(b), "l"(w), "l"(wb), "l"(np));
+    return r;
 }
 
 __device__ __forceinline__ uint64_t csub(uint64_t x, uint64_t m) { return x >= m ? x - m : x; }
@@ -57,35 +91,40 @@ struct TwMul;
 template <>
 struct TwMul<false> {
     Tw t;
-    __device__ __forceinline__ uint64_t mul(uint64_t x, uint64_t p) const { return shoup_lazy(x, t.w, t.wb, p); }
+    __device__ __forceinline__ uint64_t mul(uint64_t x, const PrimeConst& c) const
+    {
+        return shoup_lazy(x, t.w, t.wb, c.np);
+    }
 };
 template <>
 struct TwMul<true> {
     Tw fine, coarse;
-    __device__ __forceinline__ uint64_t mul(uint64_t x, uint64_t p) const
+    __device__ __forceinline__ uint64_t mul(uint64_t x, const PrimeConst& c) const
     {
-        return shoup_lazy(shoup_lazy(x, fine.w, fine.wb, p), coarse.w, coarse.wb, p);
+        return shoup_lazy(shoup_lazy(x, fine.w, fine.wb, c.np), coarse.w, coarse.wb, c.np);
     }
 };
 
-// Cooley-Tukey butterfly (Algorithm 2) in Harvey's lazy form (R9):
-// inputs and outputs in [0, 4p).
+// Cooley-Tukey butterfly (Algorithm 2) in Harvey's lazy form (R9),
+// widened for the [0,4p) multiplier: inputs and outputs in [0, 8p) (< 2^63).
+//   X <- X mod* 4p (< 4p);  T = Y w (< 4p);  X' = X + T;  Y' = X - T + 4p.
 template <class W>
-__device__ __forceinline__ void ct_bf(uint64_t& X, uint64_t& Y, const W& w, uint64_t p, uint64_t p2)
+__device__ __forceinline__ void ct_bf(uint64_t& X, uint64_t& Y, const W& w, const PrimeConst& c)
 {
-    const uint64_t x = csub(X, p2);
-    const uint64_t t = w.mul(Y, p);
+    const uint64_t x = csub(X, c.p4);
+    const uint64_t t = w.mul(Y, c);
     X = x + t;
-    Y = x - t + p2;
+    Y = x - t + c.p4;
 }
 
-// Gentleman-Sande butterfly of the inverse (R5): inputs and outputs in [0, 2p).
+// Gentleman-Sande butterfly of the inverse (R5): inputs and outputs in [0, 4p).
+//   X' = (X + Y) mod* 4p;  Y' = (X - Y + 4p) w.
 template <class W>
-__device__ __forceinline__ void gs_bf(uint64_t& X, uint64_t& Y, const W& w, uint64_t p, uint64_t p2)
+__device__ __forceinline__ void gs_bf(uint64_t& X, uint64_t& Y, const W& w, const PrimeConst& c)
 {
     const uint64_t x = X, y = Y;
-    X = csub(x + y, p2);
-    Y = w.mul(x - y + p2, p);
+    X = csub(x + y, c.p4);
+    Y = w.mul(x - y + c.p4, c);
 }
 
 __device__ __forceinline__ Tw ldg_tw(const Tw* ptr)
@@ -110,29 +149,34 @@ __device__ __forceinline__ void static_for(Fn&& f)
 // A sub-transform of size M = 2^LOGM is executed in rounds of up to 4 radix-2
 // stages (a per-thread radix-16 NTT); between rounds the
 // data is exchanged through SMEM (the "SMEM implementation").
-// Each thread holds E = 16 words (E = M below 16).
-template <int LOGM>
+// Each thread holds E = 2^LOGE words (E = M if M is smaller): rounds of
+// LOGE stages (per-thread radix-E NTTs).
+template <int LOGM, int LOGE = 4>
 struct Sched {
     static constexpr int M = 1 << LOGM;
-    static constexpr int E = LOGM < 4 ? M : 16;
-    static constexpr int NR = (LOGM + 3) / 4;
+    static constexpr int LE = LOGM < LOGE ? LOGM : LOGE;
+    static constexpr int E = 1 << LE;
+    static constexpr int NR = (LOGM + LE - 1) / LE;
     static constexpr int TB = M / E;  // threads per sub-transform
-    static constexpr int r(int i) { return (LOGM - 4 * i) < 4 ? (LOGM - 4 * i) : 4; }
+    static constexpr int r(int i) { return (LOGM - LE * i) < LE ? (LOGM - LE * i) : LE; }
+    static constexpr int S(int i) { return LE * i; }
 };
 
-// Geometry of round RI (stages [S, S+r) of the sub-transform, S = 4 RI): the
+// Geometry of round RI (stages [S, S+r) of the sub-transform, S = LE RI): the
 // thread's groups are G = qd*TB + tib; group G = (g, o) with
 //   g = G / s, o = G % s, s = M >> (S + r)  (the smallest stride),
 // and holds elements e_k = g*R*s + o + k*s, k < R = 2^r.
 // Twiddles of stage S+i of group g are Psi[((F << S) + g) << i) + h], h < 2^i,
 // F = 1 for a whole column / row, F = N1 + bb for block bb of Kernel-2.
-template <int LOGM, int RI>
+template <int LOGM, int RI, int LOGE = 4>
 struct RoundGeo {
-    static constexpr int S = 4 * RI;
-    static constexpr int r = Sched<LOGM>::r(RI);
+    using SC = Sched<LOGM, LOGE>;
+    static constexpr int S = SC::S(RI);
+    static constexpr int r = SC::r(RI);
     static constexpr int R = 1 << r;
     static constexpr int s = (1 << LOGM) >> (S + r);
-    static constexpr int GPT = Sched<LOGM>::E / R;
+    static constexpr int GPT = SC::E / R;
+    static constexpr int TB = SC::TB;
     __device__ static __forceinline__ uint32_t elem(uint32_t G, int k)
     {
         const uint32_t g = G / s, o = G % s;
@@ -141,17 +185,17 @@ struct RoundGeo {
 };
 
 // Forward round: r Cooley-Tukey stages on each of the thread's GPT groups.
-// TWF(idx) returns the TwMul for Psi index idx.  OT_FROM = first local stage
-// whose twiddles come from OT (>= LOGM: none).
-template <int LOGM, int RI, int OT_FROM, class TabF, class OtF>
+// tabf(idx) returns the table twiddle Psi[idx]; otf(idx) the OT factor pair.
+// OT_FROM = first local stage whose twiddles come from OT (>= LOGM: none).
+template <int LOGM, int LOGE, int RI, int OT_FROM, class TabF, class OtF>
 __device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32_t F, const TabF& tabf,
-                                         const OtF& otf, uint64_t p, uint64_t p2)
+                                         const OtF& otf, const PrimeConst& c)
 {
-    using Geo = RoundGeo<LOGM, RI>;
+    using Geo = RoundGeo<LOGM, RI, LOGE>;
     constexpr int R = Geo::R, S = Geo::S;
 #pragma unroll
     for (int qd = 0; qd < Geo::GPT; ++qd) {
-        const uint32_t G = qd * Sched<LOGM>::TB + tib;
+        const uint32_t G = qd * Geo::TB + tib;
         const uint32_t B = (F << S) + G / Geo::s;
 #pragma unroll
         for (int i = 0; i < Geo::r; ++i) {
@@ -163,12 +207,12 @@ __device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32
                     const TwMul<true> w = otf(idx);
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
-                        ct_bf(x[qd * R + k], x[qd * R + k + half], w, p, p2);
+                        ct_bf(x[qd * R + k], x[qd * R + k + half], w, c);
                 } else {
                     const TwMul<false> w{tabf(idx)};
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
-                        ct_bf(x[qd * R + k], x[qd * R + k + half], w, p, p2);
+                        ct_bf(x[qd * R + k], x[qd * R + k + half], w, c);
                 }
             }
         }
@@ -178,26 +222,26 @@ __device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32
 // Inverse round: the same groups and twiddle indices, Gentleman-Sande stages
 // in reverse order.  FUSE0: local stage 0 is global stage 0 (m = 1), where
 // N^-1 is fused: X' = (X+Y) N^-1, Y' = (X-Y) Psi^-1[1] N^-1 (R15).
-template <int LOGM, int RI, int OT_FROM, bool FUSE0, class TabF, class OtF>
+template <int LOGM, int LOGE, int RI, int OT_FROM, bool FUSE0, class TabF, class OtF>
 __device__ __forceinline__ void gs_round(uint64_t (&x)[16], uint32_t tib, uint32_t F, const TabF& tabf,
-                                         const OtF& otf, uint64_t p, uint64_t p2, const PrimeConst& pc)
+                                         const OtF& otf, const PrimeConst& c)
 {
-    using Geo = RoundGeo<LOGM, RI>;
+    using Geo = RoundGeo<LOGM, RI, LOGE>;
     constexpr int R = Geo::R, S = Geo::S;
 #pragma unroll
     for (int qd = 0; qd < Geo::GPT; ++qd) {
-        const uint32_t G = qd * Sched<LOGM>::TB + tib;
+        const uint32_t G = qd * Geo::TB + tib;
         const uint32_t B = (F << S) + G / Geo::s;
 #pragma unroll
         for (int i = Geo::r - 1; i >= 0; --i) {
             const int half = R >> (i + 1);
             if (FUSE0 && S + i == 0) {
-                const TwMul<false> a{pc.ninv}, b{pc.ninv_psi};
+                const TwMul<false> a{c.ninv}, b{c.ninv_psi};
 #pragma unroll
                 for (int k = 0; k < half; ++k) {
                     const uint64_t u = x[qd * R + k], v = x[qd * R + k + half];
-                    x[qd * R + k] = a.mul(u + v, p);
-                    x[qd * R + k + half] = b.mul(u - v + p2, p);
+                    x[qd * R + k] = a.mul(u + v, c);
+                    x[qd * R + k + half] = b.mul(u - v + c.p4, c);
                 }
                 continue;
             }
@@ -208,21 +252,33 @@ __device__ __forceinline__ void gs_round(uint64_t (&x)[16], uint32_t tib, uint32
                     const TwMul<true> w = otf(idx);
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
-                        gs_bf(x[qd * R + k], x[qd * R + k + half], w, p, p2);
+                        gs_bf(x[qd * R + k], x[qd * R + k + half], w, c);
                 } else {
                     const TwMul<false> w{tabf(idx)};
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
-                        gs_bf(x[qd * R + k], x[qd * R + k + half], w, p, p2);
+                        gs_bf(x[qd * R + k], x[qd * R + k + half], w, c);
                 }
             }
         }
     }
 }
 
-// SMEM swizzle for contiguous blocks: XOR bits 1..3 with bits 4..6 so the
-// round access patterns are at most 2-way bank-conflicted while 16-byte pairs
-// (2i, 2i+1) stay adjacent for vector copies.
-__device__ __forceinline__ uint32_t swz(uint32_t e) { return e ^ (((e >> 4) & 7u) << 1); }
+// Canonical reductions at the end of a direction.
+__device__ __forceinline__ uint64_t norm8(uint64_t x, const PrimeConst& c)  // [0,8p) -> [0,p)
+{
+    return csub(csub(csub(x, c.p4), c.p2), c.p);
+}
+__device__ __forceinline__ uint64_t norm4(uint64_t x, const PrimeConst& c)  // [0,4p) -> [0,p)
+{
+    return csub(csub(x, c.p2), c.p);
+}
+
+// SMEM swizzle for contiguous blocks: XOR word-address bits 1..3 with
+// (bits 4..6 ^ bits 5..7).  16-byte pairs (2i, 2i+1) stay adjacent (vector
+// copies), and every round access pattern of LOGM >= 8 -- 64-bit accesses,
+// or 128-bit ones in the stride-1 rounds -- is bank-conflict free
+// (DESIGN.md section 5.3).
+__device__ __forceinline__ uint32_t swz(uint32_t e) { return e ^ ((((e >> 4) ^ (e >> 5)) & 7u) << 1); }
 
 }  // namespace ntt

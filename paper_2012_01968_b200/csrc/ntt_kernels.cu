@@ -4,13 +4,13 @@
 //              split N = N1 * N2: the N1-point column transforms
 //              over stride-N2 columns, a 16-column tile per CTA so every global
 //              access is a full 128-byte row segment (coalescing),
-//              twiddles Psi[1..N1) preloaded into SMEM.
+//              twiddles Psi[0..N1) preloaded into SMEM.
 //   k_contig : Kernel-2 / Kernel-2' -- contiguous N2-point blocks -- and the
 //              single-kernel path for N <= 2^13, where one CTA holds whole rows.
 //              Optional on-the-fly twiddling on the last (forward)
 //              or first (inverse) 1-2 stages.
 //
-// Both run per-thread radix-16 register NTTs with SMEM exchanges between
+// Both run per-thread radix-2^LOGE register NTTs with SMEM exchanges between
 // rounds; 64-bit words, Shoup modmul.
 #include "ntt_device.cuh"
 #include "ntt_launch.h"
@@ -20,12 +20,19 @@
 namespace ntt {
 
 // ---------------------------------------------------------------- Kernel-1
-template <int LOGN1, bool INV>
-__global__ void __launch_bounds__(1 << LOGN1) k_cols(const KArgs a)
+template <int LOGN1, int LOGE>
+struct ColsCfg {
+    using SC = Sched<LOGN1, LOGE>;
+    static constexpr int CT = SC::TB * 16;  // threads: 16 columns x TB per column
+    static constexpr int MINB = CT <= 256 ? 4 : (CT <= 512 ? 2 : 1);
+    static constexpr size_t SMEM = (size_t)SC::M * 16 * 8 + (size_t)SC::M * sizeof(Tw);
+};
+
+template <int LOGN1, int LOGE, bool INV>
+__global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>::MINB) k_cols(const KArgs a)
 {
-    using SC = Sched<LOGN1>;
-    static_assert(SC::E == 16, "column kernel needs N1 >= 16");
-    constexpr int M = SC::M, NR = SC::NR;
+    using SC = Sched<LOGN1, LOGE>;
+    constexpr int M = SC::M, NR = SC::NR, CT = ColsCfg<LOGN1, LOGE>::CT;
     extern __shared__ __align__(16) uint64_t sm[];  // [M][16] words, then Tw[M]
     Tw* tws = reinterpret_cast<Tw*>(sm + M * 16);
 
@@ -38,14 +45,14 @@ __global__ void __launch_bounds__(1 << LOGN1) k_cols(const KArgs a)
     const Tw* tab = a.tab + ((uint64_t)l << a.logn);
     const PrimeConst pc = a.pc[l];
 
-    tws[tid] = ldg_tw(tab + tid);  // Psi[0..N1): the first log N1 stages' table
+    for (uint32_t i = tid; i < (uint32_t)M; i += CT) tws[i] = ldg_tw(tab + i);  // Psi[0..N1)
     __syncthreads();
     auto tabf = [&](uint32_t idx) { return tws[idx]; };
     auto otf = [&](uint32_t) { return TwMul<true>{}; };  // OT never reaches Kernel-1
 
     uint64_t x[16];
     auto g_load = [&](auto ri) {
-        using Geo = RoundGeo<LOGN1, decltype(ri)::value>;
+        using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
 #pragma unroll
         for (int qd = 0; qd < Geo::GPT; ++qd)
 #pragma unroll
@@ -53,7 +60,7 @@ __global__ void __launch_bounds__(1 << LOGN1) k_cols(const KArgs a)
                 x[qd * Geo::R + k] = col[(uint64_t)Geo::elem(qd * SC::TB + tib, k) << logn2];
     };
     auto g_store = [&](auto ri) {
-        using Geo = RoundGeo<LOGN1, decltype(ri)::value>;
+        using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
 #pragma unroll
         for (int qd = 0; qd < Geo::GPT; ++qd)
 #pragma unroll
@@ -61,14 +68,14 @@ __global__ void __launch_bounds__(1 << LOGN1) k_cols(const KArgs a)
                 col[(uint64_t)Geo::elem(qd * SC::TB + tib, k) << logn2] = x[qd * Geo::R + k];
     };
     auto s_load = [&](auto ri) {
-        using Geo = RoundGeo<LOGN1, decltype(ri)::value>;
+        using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
 #pragma unroll
         for (int qd = 0; qd < Geo::GPT; ++qd)
 #pragma unroll
             for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = sm[Geo::elem(qd * SC::TB + tib, k) * 16 + c];
     };
     auto s_store = [&](auto ri) {
-        using Geo = RoundGeo<LOGN1, decltype(ri)::value>;
+        using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
 #pragma unroll
         for (int qd = 0; qd < Geo::GPT; ++qd)
 #pragma unroll
@@ -83,9 +90,9 @@ __global__ void __launch_bounds__(1 << LOGN1) k_cols(const KArgs a)
             } else {
                 s_load(ri);
             }
-            ct_round<LOGN1, RI, 1 << 20>(x, tib, 1u, tabf, otf, pc.p, pc.p2);
+            ct_round<LOGN1, LOGE, RI, 1 << 20>(x, tib, 1u, tabf, otf, pc);
             if constexpr (RI == NR - 1) {
-                g_store(ri);
+                g_store(ri);  // [0, 8p): Kernel-2 continues the lazy chain
             } else {
                 s_store(ri);
                 __syncthreads();
@@ -100,10 +107,10 @@ __global__ void __launch_bounds__(1 << LOGN1) k_cols(const KArgs a)
             } else {
                 s_load(RC{});
             }
-            gs_round<LOGN1, RI, 1 << 20, true>(x, tib, 1u, tabf, otf, pc.p, pc.p2, pc);
+            gs_round<LOGN1, LOGE, RI, 1 << 20, true>(x, tib, 1u, tabf, otf, pc);
             if constexpr (RI == 0) {
 #pragma unroll
-                for (int k = 0; k < 16; ++k) x[k] = csub(x[k], pc.p);  // canonical [0, p)
+                for (int k = 0; k < SC::E; ++k) x[k] = norm4(x[k], pc);  // canonical [0, p)
                 g_store(RC{});
             } else {
                 s_store(RC{});
@@ -114,19 +121,21 @@ __global__ void __launch_bounds__(1 << LOGN1) k_cols(const KArgs a)
 }
 
 // ---------------------------------------------------------------- contiguous
-template <int LOGM>
+template <int LOGM, int LOGE>
 struct ContigCfg {
-    static constexpr int TB = Sched<LOGM>::TB;
+    static constexpr int TB = Sched<LOGM, LOGE>::TB;
     static constexpr int CT = TB > 256 ? TB : 256;  // threads per CTA
     static constexpr int NB = CT / TB;              // blocks per CTA iteration
     static constexpr size_t SMEM = (size_t)NB * (1 << LOGM) * 8;
+    static constexpr int MINB = CT > 256 ? 1 : (LOGE >= 4 ? 2 : 3);  // register budget
 };
 
-template <int LOGM, bool INV, bool FUSE0, int OTS>
-__global__ void __launch_bounds__(ContigCfg<LOGM>::CT) k_contig(const KArgs a)
+template <int LOGM, int LOGE, bool INV, bool FUSE0, int OTS>
+__global__ void __launch_bounds__(ContigCfg<LOGM, LOGE>::CT, ContigCfg<LOGM, LOGE>::MINB)
+    k_contig(const KArgs a)
 {
-    using SC = Sched<LOGM>;
-    using CC = ContigCfg<LOGM>;
+    using SC = Sched<LOGM, LOGE>;
+    using CC = ContigCfg<LOGM, LOGE>;
     constexpr int M = SC::M, E = SC::E, TB = SC::TB, NR = SC::NR;
     constexpr int OT_FROM = OTS ? LOGM - OTS : (1 << 20);
     extern __shared__ __align__(16) uint64_t sm[];
@@ -164,29 +173,49 @@ __global__ void __launch_bounds__(ContigCfg<LOGM>::CT) k_contig(const KArgs a)
         __syncthreads();
 
         uint64_t x[16];
+        // stride-1 rounds hold adjacent pairs (e, e+1): 128-bit SMEM accesses
         auto s_load = [&](auto ri) {
-            using Geo = RoundGeo<LOGM, decltype(ri)::value>;
+            using Geo = RoundGeo<LOGM, decltype(ri)::value, LOGE>;
 #pragma unroll
-            for (int qd = 0; qd < Geo::GPT; ++qd)
+            for (int qd = 0; qd < Geo::GPT; ++qd) {
+                if constexpr (Geo::s == 1 && Geo::R >= 2) {
 #pragma unroll
-                for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = sb[swz(Geo::elem(qd * TB + tib, k))];
+                    for (int k = 0; k < Geo::R; k += 2) {
+                        const ulonglong2 v =
+                            *reinterpret_cast<const ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k)));
+                        x[qd * Geo::R + k] = v.x;
+                        x[qd * Geo::R + k + 1] = v.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = sb[swz(Geo::elem(qd * TB + tib, k))];
+                }
+            }
         };
         auto s_store = [&](auto ri) {
-            using Geo = RoundGeo<LOGM, decltype(ri)::value>;
+            using Geo = RoundGeo<LOGM, decltype(ri)::value, LOGE>;
 #pragma unroll
-            for (int qd = 0; qd < Geo::GPT; ++qd)
+            for (int qd = 0; qd < Geo::GPT; ++qd) {
+                if constexpr (Geo::s == 1 && Geo::R >= 2) {
 #pragma unroll
-                for (int k = 0; k < Geo::R; ++k) sb[swz(Geo::elem(qd * TB + tib, k))] = x[qd * Geo::R + k];
+                    for (int k = 0; k < Geo::R; k += 2)
+                        *reinterpret_cast<ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k))) =
+                            make_ulonglong2(x[qd * Geo::R + k], x[qd * Geo::R + k + 1]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < Geo::R; ++k) sb[swz(Geo::elem(qd * TB + tib, k))] = x[qd * Geo::R + k];
+                }
+            }
         };
 
         if constexpr (!INV) {
             static_for<NR>([&](auto ri) {
                 constexpr int RI = decltype(ri)::value;
                 s_load(ri);
-                ct_round<LOGM, RI, OT_FROM>(x, tib, F, tabf, otf, pc.p, pc.p2);
+                ct_round<LOGM, LOGE, RI, OT_FROM>(x, tib, F, tabf, otf, pc);
                 if constexpr (RI == NR - 1) {
 #pragma unroll
-                    for (int k = 0; k < E; ++k) x[k] = csub(csub(x[k], pc.p2), pc.p);  // [0,4p) -> [0,p)
+                    for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // [0,8p) -> [0,p)
                 }
                 s_store(ri);
                 __syncthreads();
@@ -196,10 +225,10 @@ __global__ void __launch_bounds__(ContigCfg<LOGM>::CT) k_contig(const KArgs a)
                 constexpr int RI = NR - 1 - decltype(rj)::value;
                 using RC = std::integral_constant<int, RI>;
                 s_load(RC{});
-                gs_round<LOGM, RI, OT_FROM, FUSE0>(x, tib, F, tabf, otf, pc.p, pc.p2, pc);
+                gs_round<LOGM, LOGE, RI, OT_FROM, FUSE0>(x, tib, F, tabf, otf, pc);
                 if constexpr (FUSE0 && RI == 0) {
 #pragma unroll
-                    for (int k = 0; k < E; ++k) x[k] = csub(x[k], pc.p);
+                    for (int k = 0; k < E; ++k) x[k] = norm4(x[k], pc);
                 }
                 s_store(RC{});
                 __syncthreads();
@@ -230,24 +259,23 @@ bool set_once(std::atomic<uint64_t>& mask)
     return mask.fetch_or(bit) & bit;
 }
 
-template <int LOGN1, bool INV>
+template <int LOGN1, int LOGE, bool INV>
 cudaError_t launch_cols_t(const KArgs& a, uint32_t rows, cudaStream_t st)
 {
-    constexpr int M = 1 << LOGN1;
-    const size_t smem = (size_t)M * 16 * 8 + (size_t)M * sizeof(Tw);
-    auto fn = k_cols<LOGN1, INV>;
+    using CC = ColsCfg<LOGN1, LOGE>;
+    auto fn = k_cols<LOGN1, LOGE, INV>;
     static std::atomic<uint64_t> attr_set{0};  // one bit per device
-    if (!set_once(attr_set)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (!set_once(attr_set)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
     const uint64_t grid = (uint64_t)rows << a.log_tiles;
-    fn<<<(unsigned)grid, M, smem, st>>>(a);
+    fn<<<(unsigned)grid, CC::CT, CC::SMEM, st>>>(a);
     return cudaPeekAtLastError();
 }
 
-template <int LOGM, bool INV, bool FUSE0, int OTS>
+template <int LOGM, int LOGE, bool INV, bool FUSE0, int OTS>
 cudaError_t launch_contig_t(KArgs a, uint32_t iters, cudaStream_t st)
 {
-    using CC = ContigCfg<LOGM>;
-    auto fn = k_contig<LOGM, INV, FUSE0, OTS>;
+    using CC = ContigCfg<LOGM, LOGE>;
+    auto fn = k_contig<LOGM, LOGE, INV, FUSE0, OTS>;
     static std::atomic<uint64_t> attr_set{0};  // one bit per device
     if (!set_once(attr_set)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
     a.iters = iters;
@@ -257,30 +285,30 @@ cudaError_t launch_contig_t(KArgs a, uint32_t iters, cudaStream_t st)
     return cudaPeekAtLastError();
 }
 
-template <int LOGM, bool INV, bool FUSE0>
+template <int LOGM, int LOGE, bool INV, bool FUSE0>
 cudaError_t launch_contig_ot(const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
 {
     switch (ots) {
-        case 0: return launch_contig_t<LOGM, INV, FUSE0, 0>(a, iters, st);
-        case 1: return launch_contig_t<LOGM, INV, FUSE0, (LOGM >= 1 ? 1 : 0)>(a, iters, st);
-        default: return launch_contig_t<LOGM, INV, FUSE0, (LOGM >= 2 ? 2 : LOGM)>(a, iters, st);
+        case 0: return launch_contig_t<LOGM, LOGE, INV, FUSE0, 0>(a, iters, st);
+        case 1: return launch_contig_t<LOGM, LOGE, INV, FUSE0, 1>(a, iters, st);
+        default: return launch_contig_t<LOGM, LOGE, INV, FUSE0, (LOGM >= 2 ? 2 : LOGM)>(a, iters, st);
     }
 }
 
-template <bool INV, bool FUSE0, int... Ls>
+template <int LOGE, bool INV, bool FUSE0, int... Ls>
 cudaError_t contig_switch(int logm, const KArgs& a, int ots, uint32_t iters, cudaStream_t st,
                           std::integer_sequence<int, Ls...>)
 {
     cudaError_t err = cudaErrorInvalidValue;
-    ((logm == Ls ? (err = launch_contig_ot<Ls, INV, FUSE0>(a, ots, iters, st), 0) : 0), ...);
+    ((logm == Ls ? (err = launch_contig_ot<Ls, LOGE, INV, FUSE0>(a, ots, iters, st), 0) : 0), ...);
     return err;
 }
 
-template <bool INV, int... Ls>
+template <int LOGE, bool INV, int... Ls>
 cudaError_t cols_switch(int logn1, const KArgs& a, uint32_t rows, cudaStream_t st, std::integer_sequence<int, Ls...>)
 {
     cudaError_t err = cudaErrorInvalidValue;
-    ((logn1 == Ls ? (err = launch_cols_t<Ls, INV>(a, rows, st), 0) : 0), ...);
+    ((logn1 == Ls ? (err = launch_cols_t<Ls, LOGE, INV>(a, rows, st), 0) : 0), ...);
     return err;
 }
 
@@ -293,21 +321,27 @@ using K1Sizes = std::integer_sequence<int, 6, 7, 8, 9, 10>;
 
 cudaError_t launch_single(bool inverse, const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
 {
-    return inverse ? contig_switch<true, true>((int)a.logn, a, ots, iters, st, SingleSizes{})
-                   : contig_switch<false, false>((int)a.logn, a, ots, iters, st, SingleSizes{});
+    return inverse ? contig_switch<4, true, true>((int)a.logn, a, ots, iters, st, SingleSizes{})
+                   : contig_switch<4, false, false>((int)a.logn, a, ots, iters, st, SingleSizes{});
 }
 
-cudaError_t launch_k2(bool inverse, const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
+cudaError_t launch_k2(bool inverse, int loge, const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
 {
     const int logm = (int)(a.logn - a.log_n1);
-    return inverse ? contig_switch<true, false>(logm, a, ots, iters, st, K2Sizes{})
-                   : contig_switch<false, false>(logm, a, ots, iters, st, K2Sizes{});
+    if (loge == 3)
+        return inverse ? contig_switch<3, true, false>(logm, a, ots, iters, st, K2Sizes{})
+                       : contig_switch<3, false, false>(logm, a, ots, iters, st, K2Sizes{});
+    return inverse ? contig_switch<4, true, false>(logm, a, ots, iters, st, K2Sizes{})
+                   : contig_switch<4, false, false>(logm, a, ots, iters, st, K2Sizes{});
 }
 
-cudaError_t launch_k1(bool inverse, const KArgs& a, uint32_t rows, cudaStream_t st)
+cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st)
 {
-    return inverse ? cols_switch<true>((int)a.log_n1, a, rows, st, K1Sizes{})
-                   : cols_switch<false>((int)a.log_n1, a, rows, st, K1Sizes{});
+    if (loge == 3)
+        return inverse ? cols_switch<3, true>((int)a.log_n1, a, rows, st, K1Sizes{})
+                       : cols_switch<3, false>((int)a.log_n1, a, rows, st, K1Sizes{});
+    return inverse ? cols_switch<4, true>((int)a.log_n1, a, rows, st, K1Sizes{})
+                   : cols_switch<4, false>((int)a.log_n1, a, rows, st, K1Sizes{});
 }
 
 }  // namespace ntt

@@ -8,7 +8,8 @@ namespace ntt {
 // One kernel per row: contiguous rows of N = 2^logn, N <= 2^13.
 cudaError_t launch_single(bool inverse, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
 // Kernel-2 (forward) / Kernel-2' (inverse): contiguous N2-blocks.
-cudaError_t launch_k2(bool inverse, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
+// loge: per-thread radix 2^loge (3 or 4).
+cudaError_t launch_k2(bool inverse, int loge, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
 // Kernel-1 (forward) / Kernel-1' (inverse): stride-N2 columns, 16 per CTA.
-cudaError_t launch_k1(bool inverse, const KArgs& a, uint32_t rows, cudaStream_t st);
+cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st);
 }  // namespace ntt

@@ -105,6 +105,93 @@ __global__ void k_shoup(uint64_t* out, uint64_t p, uint64_t w, uint64_t wb) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// ---- butterfly variants (V0 exact __umul64hi; V1 truncated quotient; V2 truncated + (-p))
+__device__ __forceinline__ uint64_t shoup_trunc(uint64_t b, uint64_t w, uint64_t wb, uint64_t p) {
+  uint32_t b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32), v0 = (uint32_t)wb, v1 = (uint32_t)(wb >> 32);
+  uint64_t q = (uint64_t)b1 * v1 + __umulhi(b1, v0) + __umulhi(b0, v1);
+  return b * w - q * p;
+}
+__device__ __forceinline__ uint64_t shoup_trunc_np(uint64_t b, uint64_t w, uint64_t wb, uint64_t np) {
+  uint32_t b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32), v0 = (uint32_t)wb, v1 = (uint32_t)(wb >> 32);
+  uint64_t q = (uint64_t)b1 * v1 + __umulhi(b1, v0) + __umulhi(b0, v1);
+  return b * w + q * np;
+}
+// Shoup with the quotient and remainder in hand-written PTX (adds via add.cc/addc)
+__device__ __forceinline__ uint64_t shoup_ptx(uint64_t b, uint64_t w, uint64_t wb, uint64_t np) {
+  uint64_t r;
+  asm("{\n\t"
+      ".reg .u32 b0, b1, v0, v1, w0, w1, n0, n1, t0, t1, q0, q1, r0, r1;\n\t"
+      ".reg .u64 q, a;\n\t"
+      "mov.b64 {b0, b1}, %1;\n\t"
+      "mov.b64 {w0, w1}, %2;\n\t"
+      "mov.b64 {v0, v1}, %3;\n\t"
+      "mov.b64 {n0, n1}, %4;\n\t"
+      "mul.hi.u32 t0, b1, v0;\n\t"
+      "mul.hi.u32 t1, b0, v1;\n\t"
+      "mul.wide.u32 q, b1, v1;\n\t"
+      "mov.b64 {q0, q1}, q;\n\t"
+      "add.cc.u32 q0, q0, t0;\n\t"
+      "addc.u32 q1, q1, 0;\n\t"
+      "add.cc.u32 q0, q0, t1;\n\t"
+      "addc.u32 q1, q1, 0;\n\t"
+      "mul.wide.u32 a, b0, w0;\n\t"
+      "mov.b64 {r0, r1}, a;\n\t"
+      "mad.lo.u32 r1, b0, w1, r1;\n\t"
+      "mad.lo.u32 r1, b1, w0, r1;\n\t"
+      "mad.lo.u32 r1, q0, n1, r1;\n\t"
+      "mad.lo.u32 r1, q1, n0, r1;\n\t"
+      "mov.b64 a, {r0, r1};\n\t"
+      "mad.wide.u32 a, q0, n0, a;\n\t"
+      "mov.b64 %0, a;\n\t"
+      "}" : "=l"(r) : "l"(b), "l"(w), "l"(wb), "l"(np));
+  return r;
+}
+template <int V>
+__global__ void k_bfv(uint64_t* out, uint64_t p, uint64_t w, uint64_t wb) {
+  uint64_t X[CH], Y[CH];
+  for (int c = 0; c < CH; ++c) { X[c] = (threadIdx.x * 77 + c) % p; Y[c] = (threadIdx.x * 31 + c * 5) % p; }
+  const uint64_t p4 = 4 * p, np = 0 - p, p2 = 2 * p;
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if (V == 0) {
+        uint64_t x = X[c] >= p2 ? X[c] - p2 : X[c];
+        uint64_t t = shoup_lazy(Y[c], w, wb, p);
+        X[c] = x + t; Y[c] = x - t + p2;
+      } else {
+        uint64_t x = X[c] >= p4 ? X[c] - p4 : X[c];
+        uint64_t t = V == 1 ? shoup_trunc(Y[c], w, wb, p) : V == 2 ? shoup_trunc_np(Y[c], w, wb, np)
+                                                          : shoup_ptx(Y[c], w, wb, np);
+        X[c] = x + t; Y[c] = x - t + p4;
+      }
+    }
+  uint64_t s = 0;
+  for (int c = 0; c < CH; ++c) s ^= X[c] ^ Y[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+// GS butterflies: exact and truncated
+template <int V>
+__global__ void k_gsv(uint64_t* out, uint64_t p, uint64_t w, uint64_t wb) {
+  uint64_t X[CH], Y[CH];
+  for (int c = 0; c < CH; ++c) { X[c] = (threadIdx.x * 77 + c) % p; Y[c] = (threadIdx.x * 31 + c * 5) % p; }
+  const uint64_t p4 = 4 * p, np = 0 - p, p2 = 2 * p;
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const uint64_t x = X[c], y = Y[c];
+      if (V == 0) {
+        uint64_t s = x + y; X[c] = s >= p2 ? s - p2 : s;
+        Y[c] = shoup_lazy(x - y + p2, w, wb, p);
+      } else {
+        uint64_t s = x + y; X[c] = s >= p4 ? s - p4 : s;
+        Y[c] = V == 1 ? shoup_trunc_np(x - y + p4, w, wb, np) : shoup_ptx(x - y + p4, w, wb, np);
+      }
+    }
+  uint64_t s = 0;
+  for (int c = 0; c < CH; ++c) s ^= X[c] ^ Y[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 typedef void (*kfun32)(uint64_t*, uint32_t, uint32_t);
 typedef void (*kfun64)(uint64_t*, uint64_t, uint64_t, uint64_t);
 
@@ -139,7 +226,9 @@ int main() {
   }
   uint64_t p = 1152921504606584833ull, w = 30403152079314ull;
   uint64_t wb = (uint64_t)(((unsigned __int128)w << 64) / p);
-  struct { const char* name; kfun64 f; } k64[] = {{"butterfly_ct_harvey", k_bf_ct}, {"shoup_lazy", k_shoup}};
+  struct { const char* name; kfun64 f; } k64[] = {{"butterfly_ct_harvey", k_bf_ct}, {"shoup_lazy", k_shoup},
+      {"ct_v0_exact", k_bfv<0>}, {"ct_v1_trunc", k_bfv<1>}, {"ct_v2_trunc_np", k_bfv<2>}, {"ct_v3_ptx", k_bfv<3>},
+      {"gs_v0_exact", k_gsv<0>}, {"gs_v1_trunc_np", k_gsv<1>}, {"gs_v2_ptx", k_gsv<2>}};
   for (auto& k : k64) {
     for (int rep = 0; rep < 3; ++rep) k.f<<<blocks, threads>>>(out, p, w, wb);
     cudaEventRecord(e0);
@@ -151,6 +240,20 @@ int main() {
     double ops = (double)blocks * threads * ITERS * CH;
     printf("{\"kernel\": \"%s\", \"ms\": %.4f, \"Gops_per_s\": %.1f, \"ops_per_ns_per_sm\": %.3f}\n", k.name, ms,
            ops / ms / 1e6, ops / ms / 1e6 / sms);
+  }
+  // occupancy sweep for the PTX butterfly: warps per SM vs rate
+  for (int wps : {4, 8, 12, 16, 24, 32, 48, 64}) {
+    int thr = 128, bps = wps * 32 / thr;
+    int nb = sms * bps;
+    for (int rep = 0; rep < 2; ++rep) k_bfv<3><<<nb, thr>>>(out, p, w, wb);
+    cudaEventRecord(e0);
+    k_bfv<3><<<nb, thr>>>(out, p, w, wb);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double ops = (double)nb * thr * ITERS * CH;
+    printf("{\"kernel\": \"ct_v3_ptx_occ\", \"warps_per_sm\": %d, \"Gops_per_s\": %.1f}\n", wps, ops / ms / 1e6);
   }
   return 0;
 }
