@@ -291,6 +291,9 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
                 c.p2 = 2 * q;
                 c.p4 = 4 * q;
                 c.np = 0 - q;
+                c.p5 = 5 * q;
+                c.p4_hi = (uint32_t)((4 * q) >> 32);
+                c.pad = 0;
                 nttp::Twiddle t1 = nttp::shoup_pair(ninv, q), t2 = nttp::shoup_pair(ninv_psi, q);
                 c.ninv = Tw{t1.w, t1.wb};
                 c.ninv_psi = Tw{t2.w, t2.wb};

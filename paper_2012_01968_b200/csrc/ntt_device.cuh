@@ -20,6 +20,8 @@ struct __align__(16) Tw {
 struct __align__(16) PrimeConst {
     uint64_t p, p2, p4;  // p, 2p, 4p
     uint64_t np;         // 2^64 - p
+    uint64_t p5;         // 5p: the GS difference offset (section 5.1)
+    uint32_t p4_hi, pad;  // high word of 4p
     Tw ninv;             // N^-1
     Tw ninv_psi;         // N^-1 * Psi^-1[1], the fused last GS stage (R15)
 };
@@ -47,7 +49,8 @@ struct KArgs {
 // <= q' + 2 and, with Shoup's own bound, floor(b w / p) - q' in [0, 3]:
 //   r = b w - q' p = (b w mod p) + k p,  k in {0,1,2,3}  ->  r in [0, 4p).
 // r is formed mod 2^64 as b w + q' (2^64 - p): 3 IMAD.WIDE, 2 IMAD.HI and
-// 4 IMAD on the multiply pipe.  np = 2^64 - p.
+// 4 IMAD on the multiply pipe.  np = 2^64 - p.  The 64-bit partial product
+// b0 w0 + q0 n0 is accumulated in one register pair (no re-pairing moves).
 __device__ __forceinline__ uint64_t shoup_lazy(uint64_t b, uint64_t w, uint64_t wb, uint64_t np)
 {
     uint64_t r;
@@ -67,14 +70,13 @@ __device__ __forceinline__ uint64_t shoup_lazy(uint64_t b, uint64_t w, uint64_t 
         "add.cc.u32 q0, q0, t1;\n\t"
         "addc.u32 q1, q1, 0;\n\t"
         "mul.wide.u32 a, b0, w0;\n\t"
+        "mad.wide.u32 a, q0, n0, a;\n\t"
         "mov.b64 {r0, r1}, a;\n\t"
         "mad.lo.u32 r1, b0, w1, r1;\n\t"
         "mad.lo.u32 r1, b1, w0, r1;\n\t"
         "mad.lo.u32 r1, q0, n1, r1;\n\t"
         "mad.lo.u32 r1, q1, n0, r1;\n\t"
-        "mov.b64 a, {r0, r1};\n\t"
-        "mad.wide.u32 a, q0, n0, a;\n\t"
-        "mov.b64 %0, a;\n\t"
+        "mov.b64 %0, {r0, r1};\n\t"
         "}"
         : "=l"(r)
         : "l"(b), "l"(w), "l"(wb), "l"(np));
@@ -82,6 +84,15 @@ __device__ __forceinline__ uint64_t shoup_lazy(uint64_t b, uint64_t w, uint64_t 
 }
 
 __device__ __forceinline__ uint64_t csub(uint64_t x, uint64_t m) { return x >= m ? x - m : x; }
+
+// Conditional subtraction decided on the high words only: subtracts m iff
+// hi(x) > hi(m) (then x > m).  The result is < max(x - m, m + 2^32): an
+// excess of at most 2^32 over the exact reduction, absorbed by the bounds of
+// section 5.1 and removed by the final exact normalisation.
+__device__ __forceinline__ uint64_t csub_hi(uint64_t x, uint64_t m, uint32_t m_hi)
+{
+    return (uint32_t)(x >> 32) > m_hi ? x - m : x;
+}
 
 // The twiddle of one butterfly group: a table entry (one Shoup multiply) or,
 // under on-the-fly twiddling, the pair (w1, w2) whose product is
@@ -106,25 +117,26 @@ struct TwMul<true> {
 };
 
 // Cooley-Tukey butterfly (Algorithm 2) in Harvey's lazy form (R9),
-// widened for the [0,4p) multiplier: inputs and outputs in [0, 8p) (< 2^63).
-//   X <- X mod* 4p (< 4p);  T = Y w (< 4p);  X' = X + T;  Y' = X - T + 4p.
+// widened for the [0,4p) multiplier: inputs and outputs in [0, 8p + 2^32).
+//   X <- X mod* 4p (< 4p + 2^32);  T = Y w (< 4p);  X' = X + T;  Y' = X - T + 4p.
 template <class W>
 __device__ __forceinline__ void ct_bf(uint64_t& X, uint64_t& Y, const W& w, const PrimeConst& c)
 {
-    const uint64_t x = csub(X, c.p4);
+    const uint64_t x = csub_hi(X, c.p4, c.p4_hi);
     const uint64_t t = w.mul(Y, c);
     X = x + t;
     Y = x - t + c.p4;
 }
 
-// Gentleman-Sande butterfly of the inverse (R5): inputs and outputs in [0, 4p).
-//   X' = (X + Y) mod* 4p;  Y' = (X - Y + 4p) w.
+// Gentleman-Sande butterfly of the inverse (R5): inputs and outputs below
+// 4p + 2^(32+s) after s stages (< 4p + 2^49 for N <= 2^17).
+//   X' = (X + Y) mod* 4p;  Y' = (X - Y + 5p) w  (5p > any Y, so no wrap).
 template <class W>
 __device__ __forceinline__ void gs_bf(uint64_t& X, uint64_t& Y, const W& w, const PrimeConst& c)
 {
     const uint64_t x = X, y = Y;
-    X = csub(x + y, c.p4);
-    Y = w.mul(x - y + c.p4, c);
+    X = csub_hi(x + y, c.p4, c.p4_hi);
+    Y = w.mul(x - y + c.p5, c);
 }
 
 __device__ __forceinline__ Tw ldg_tw(const Tw* ptr)
@@ -241,7 +253,7 @@ __device__ __forceinline__ void gs_round(uint64_t (&x)[16], uint32_t tib, uint32
                 for (int k = 0; k < half; ++k) {
                     const uint64_t u = x[qd * R + k], v = x[qd * R + k + half];
                     x[qd * R + k] = a.mul(u + v, c);
-                    x[qd * R + k + half] = b.mul(u - v + c.p4, c);
+                    x[qd * R + k + half] = b.mul(u - v + c.p5, c);
                 }
                 continue;
             }
@@ -265,9 +277,9 @@ __device__ __forceinline__ void gs_round(uint64_t (&x)[16], uint32_t tib, uint32
 }
 
 // Canonical reductions at the end of a direction.
-__device__ __forceinline__ uint64_t norm8(uint64_t x, const PrimeConst& c)  // [0,8p) -> [0,p)
+__device__ __forceinline__ uint64_t norm8(uint64_t x, const PrimeConst& c)  // [0,8p+2^32) -> [0,p)
 {
-    return csub(csub(csub(x, c.p4), c.p2), c.p);
+    return csub(csub(csub(csub(x, c.p4), c.p2), c.p), c.p);
 }
 __device__ __forceinline__ uint64_t norm4(uint64_t x, const PrimeConst& c)  // [0,4p) -> [0,p)
 {

@@ -28,7 +28,7 @@ struct ColsCfg {
     static constexpr size_t SMEM = (size_t)SC::M * 16 * 8 + (size_t)SC::M * sizeof(Tw);
 };
 
-template <int LOGN1, int LOGE, bool INV>
+template <int LOGN1, int LOGN, int LOGE, bool INV>
 __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>::MINB) k_cols(const KArgs a)
 {
     using SC = Sched<LOGN1, LOGE>;
@@ -40,9 +40,9 @@ __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>
     const uint32_t tile = blockIdx.x & ((1u << a.log_tiles) - 1u);
     const uint32_t q = blockIdx.x >> a.log_tiles;  // prime-major: q = l * batch + b
     const uint32_t l = q / a.batch, b = q - l * a.batch;
-    const uint32_t logn2 = a.logn - LOGN1;
-    uint64_t* col = a.data + (((uint64_t)b * a.L + l) << a.logn) + tile * 16u + c;
-    const Tw* tab = a.tab + ((uint64_t)l << a.logn);
+    constexpr uint32_t logn2 = LOGN - LOGN1;  // compile-time stride: immediate offsets
+    uint64_t* col = a.data + (((uint64_t)b * a.L + l) << LOGN) + tile * 16u + c;
+    const Tw* tab = a.tab + ((uint64_t)l << LOGN);
     const PrimeConst pc = a.pc[l];
 
     for (uint32_t i = tid; i < (uint32_t)M; i += CT) tws[i] = ldg_tw(tab + i);  // Psi[0..N1)
@@ -130,6 +130,19 @@ struct ContigCfg {
     static constexpr int MINB = CT > 256 ? 1 : (LOGE >= 4 ? 2 : 3);  // register budget
 };
 
+// Barrier over the TB threads of one block: blocks never share SMEM, so a
+// block that fits one warp synchronises with __syncwarp and larger blocks with
+// a named barrier of their own; CTA-wide barriers are avoided.
+template <int TB>
+__device__ __forceinline__ void block_sync(uint32_t blk)
+{
+    if constexpr (TB <= 32) {
+        __syncwarp();
+    } else {
+        asm volatile("bar.sync %0, %1;" ::"r"(blk + 1), "n"(TB) : "memory");
+    }
+}
+
 template <int LOGM, int LOGE, bool INV, bool FUSE0, int OTS>
 __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE>::CT, ContigCfg<LOGM, LOGE>::MINB)
     k_contig(const KArgs a)
@@ -170,7 +183,7 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE>::CT, ContigCfg<LOGM, LOG
             const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(g + 2 * ch);
             *reinterpret_cast<ulonglong2*>(sb + swz(2 * ch)) = v;
         }
-        __syncthreads();
+        block_sync<TB>(blk);
 
         uint64_t x[16];
         // stride-1 rounds hold adjacent pairs (e, e+1): 128-bit SMEM accesses
@@ -218,7 +231,7 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE>::CT, ContigCfg<LOGM, LOG
                     for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // [0,8p) -> [0,p)
                 }
                 s_store(ri);
-                __syncthreads();
+                block_sync<TB>(blk);
             });
         } else {
             static_for<NR>([&](auto rj) {
@@ -231,7 +244,7 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE>::CT, ContigCfg<LOGM, LOG
                     for (int k = 0; k < E; ++k) x[k] = norm4(x[k], pc);
                 }
                 s_store(RC{});
-                __syncthreads();
+                block_sync<TB>(blk);
             });
         }
 
@@ -243,7 +256,7 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE>::CT, ContigCfg<LOGM, LOG
                 *reinterpret_cast<ulonglong2*>(g + 2 * ch) = *reinterpret_cast<const ulonglong2*>(sb + swz(2 * ch));
             }
         }
-        __syncthreads();
+        block_sync<TB>(blk);
     }
 }
 
@@ -259,11 +272,11 @@ bool set_once(std::atomic<uint64_t>& mask)
     return mask.fetch_or(bit) & bit;
 }
 
-template <int LOGN1, int LOGE, bool INV>
+template <int LOGN1, int LOGN, int LOGE, bool INV>
 cudaError_t launch_cols_t(const KArgs& a, uint32_t rows, cudaStream_t st)
 {
     using CC = ColsCfg<LOGN1, LOGE>;
-    auto fn = k_cols<LOGN1, LOGE, INV>;
+    auto fn = k_cols<LOGN1, LOGN, LOGE, INV>;
     static std::atomic<uint64_t> attr_set{0};  // one bit per device
     if (!set_once(attr_set)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
     const uint64_t grid = (uint64_t)rows << a.log_tiles;
@@ -304,20 +317,25 @@ cudaError_t contig_switch(int logm, const KArgs& a, int ots, uint32_t iters, cud
     return err;
 }
 
-template <int LOGE, bool INV, int... Ls>
-cudaError_t cols_switch(int logn1, const KArgs& a, uint32_t rows, cudaStream_t st, std::integer_sequence<int, Ls...>)
+// Ks encodes (logn << 4) | log_n1
+template <int LOGE, bool INV, int... Ks>
+cudaError_t cols_switch(int key, const KArgs& a, uint32_t rows, cudaStream_t st, std::integer_sequence<int, Ks...>)
 {
     cudaError_t err = cudaErrorInvalidValue;
-    ((logn1 == Ls ? (err = launch_cols_t<Ls, LOGE, INV>(a, rows, st), 0) : 0), ...);
+    ((key == Ks ? (err = launch_cols_t<(Ks & 15), (Ks >> 4), LOGE, INV>(a, rows, st), 0) : 0), ...);
     return err;
 }
 
 }  // namespace
 
-// Supported sizes: single kernel LOGM 1..13; Kernel-2 LOGM 6..11; Kernel-1 LOGN1 6..10.
+// Supported sizes: single kernel LOGM 1..13; Kernel-2 LOGM 6..11; Kernel-1 (logn, log_n1) pairs below.
 using SingleSizes = std::integer_sequence<int, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13>;
 using K2Sizes = std::integer_sequence<int, 6, 7, 8, 9, 10, 11>;
-using K1Sizes = std::integer_sequence<int, 6, 7, 8, 9, 10>;
+#define K1P(n, n1) (((n) << 4) | (n1))
+using K1Pairs = std::integer_sequence<int, K1P(14, 6), K1P(14, 7), K1P(14, 8), K1P(15, 6), K1P(15, 7), K1P(15, 8),
+                                      K1P(15, 9), K1P(16, 6), K1P(16, 7), K1P(16, 8), K1P(16, 9), K1P(16, 10),
+                                      K1P(17, 6), K1P(17, 7), K1P(17, 8), K1P(17, 9), K1P(17, 10)>;
+#undef K1P
 
 cudaError_t launch_single(bool inverse, const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
 {
@@ -337,11 +355,10 @@ cudaError_t launch_k2(bool inverse, int loge, const KArgs& a, int ots, uint32_t 
 
 cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st)
 {
-    if (loge == 3)
-        return inverse ? cols_switch<3, true>((int)a.log_n1, a, rows, st, K1Sizes{})
-                       : cols_switch<3, false>((int)a.log_n1, a, rows, st, K1Sizes{});
-    return inverse ? cols_switch<4, true>((int)a.log_n1, a, rows, st, K1Sizes{})
-                   : cols_switch<4, false>((int)a.log_n1, a, rows, st, K1Sizes{});
+    (void)loge;  // Kernel-1 runs per-thread radix 16 (the measured best, profiles/)
+    const int key = (int)((a.logn << 4) | a.log_n1);
+    return inverse ? cols_switch<4, true>(key, a, rows, st, K1Pairs{})
+                   : cols_switch<4, false>(key, a, rows, st, K1Pairs{});
 }
 
 }  // namespace ntt
