@@ -197,7 +197,8 @@ struct RoundGeo {
 };
 
 // Forward round: r Cooley-Tukey stages on each of the thread's GPT groups.
-// tabf(idx) returns the table twiddle Psi[idx]; otf(idx) the OT factor pair.
+// tabf(idx, j) returns the table twiddle Psi[idx] of local stage j; otf(idx)
+// the OT factor pair.
 // OT_FROM = first local stage whose twiddles come from OT (>= LOGM: none).
 template <int LOGM, int LOGE, int RI, int OT_FROM, class TabF, class OtF>
 __device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32_t F, const TabF& tabf,
@@ -221,7 +222,7 @@ __device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
                         ct_bf(x[qd * R + k], x[qd * R + k + half], w, c);
                 } else {
-                    const TwMul<false> w{tabf(idx)};
+                    const TwMul<false> w{tabf(idx, S + i)};
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
                         ct_bf(x[qd * R + k], x[qd * R + k + half], w, c);
@@ -266,7 +267,7 @@ __device__ __forceinline__ void gs_round(uint64_t (&x)[16], uint32_t tib, uint32
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
                         gs_bf(x[qd * R + k], x[qd * R + k + half], w, c);
                 } else {
-                    const TwMul<false> w{tabf(idx)};
+                    const TwMul<false> w{tabf(idx, S + i)};
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
                         gs_bf(x[qd * R + k], x[qd * R + k + half], w, c);

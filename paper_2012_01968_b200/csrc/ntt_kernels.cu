@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>
 
     for (uint32_t i = tid; i < (uint32_t)M; i += CT) tws[i] = ldg_tw(tab + i);  // Psi[0..N1)
     __syncthreads();
-    auto tabf = [&](uint32_t idx) { return tws[idx]; };
+    auto tabf = [&](uint32_t idx, int) { return tws[idx]; };
     auto otf = [&](uint32_t) { return TwMul<true>{}; };  // OT never reaches Kernel-1
 
     uint64_t x[16];
@@ -121,14 +121,23 @@ __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>
 }
 
 // ---------------------------------------------------------------- contiguous
-template <int LOGM, int LOGE>
+template <int LOGM, int LOGE, bool TWS = false>
 struct ContigCfg {
     static constexpr int TB = Sched<LOGM, LOGE>::TB;
     static constexpr int CT = TB > 256 ? TB : 256;  // threads per CTA
     static constexpr int NB = CT / TB;              // blocks per CTA iteration
-    static constexpr size_t SMEM = (size_t)NB * (1 << LOGM) * 8;
+    // data words, plus (TWS) each block's local twiddle table of M entries
+    static constexpr size_t SMEM = (size_t)NB * (1 << LOGM) * (8 + (TWS ? sizeof(Tw) : 0));
     static constexpr int MINB = CT > 256 ? 1 : (LOGE >= 4 ? 2 : 3);  // register budget
 };
+
+// 16-byte asynchronous global -> shared copy (LDGSTS), and its completion.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
+{
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Barrier over the TB threads of one block: blocks never share SMEM, so a
 // block that fits one warp synchronises with __syncwarp and larger blocks with
@@ -143,18 +152,24 @@ __device__ __forceinline__ void block_sync(uint32_t blk)
     }
 }
 
-template <int LOGM, int LOGE, bool INV, bool FUSE0, int OTS>
-__global__ void __launch_bounds__(ContigCfg<LOGM, LOGE>::CT, ContigCfg<LOGM, LOGE>::MINB)
+// TWS: stage each block's twiddles in SMEM.  Block bb of Kernel-2 (F = N1+bb)
+// uses Psi[F 2^j + h], h < 2^j, at local stage j: M-1 entries in log M
+// contiguous table ranges, copied with cp.async into a local table
+// tl[2^j + h] at the block's start (one latency per block instead of one per
+// round) and read back with LDS.128.  Stages under OT skip their ranges.
+template <int LOGM, int LOGE, bool INV, bool FUSE0, int OTS, bool TWS>
+__global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM, LOGE, TWS>::MINB)
     k_contig(const KArgs a)
 {
     using SC = Sched<LOGM, LOGE>;
-    using CC = ContigCfg<LOGM, LOGE>;
+    using CC = ContigCfg<LOGM, LOGE, TWS>;
     constexpr int M = SC::M, E = SC::E, TB = SC::TB, NR = SC::NR;
     constexpr int OT_FROM = OTS ? LOGM - OTS : (1 << 20);
     extern __shared__ __align__(16) uint64_t sm[];
 
     const uint32_t tid = threadIdx.x, blk = tid / TB, tib = tid % TB;
     uint64_t* sb = sm + blk * M;
+    Tw* tl = reinterpret_cast<Tw*>(sm + CC::NB * M) + blk * M;
     const uint32_t n1mask = (1u << a.log_n1) - 1u;
     const uint32_t B_ot = 1u << a.ot_logb;
 
@@ -169,23 +184,75 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE>::CT, ContigCfg<LOGM, LOG
         const Tw* tab = a.tab + ((uint64_t)l << a.logn);
         const Tw* ot = a.ot + (uint64_t)l * (B_ot + ((1u << a.logn) >> a.ot_logb));
         const PrimeConst pc = a.pc[l];
-        auto tabf = [&](uint32_t idx) { return ldg_tw(tab + idx); };
+        if constexpr (TWS) {
+            // local stages j < OT_FROM: tl[2^j + h] <- Psi[F 2^j + h]
+            constexpr int NT = (OT_FROM < LOGM ? (1 << OT_FROM) : M) - 1;  // entries 1..NT
+#pragma unroll
+            for (int u = 0; u < (NT + TB - 1) / TB; ++u) {
+                const uint32_t t = 1 + u * TB + tib;
+                if (t <= (uint32_t)NT) {
+                    const uint32_t j = 31 - __clz(t), h = t - (1u << j);
+                    cp_async16(tl + t, tab + ((F << j) + h));
+                }
+            }
+        }
+        auto tabf = [&](uint32_t idx, int j) {
+            if constexpr (TWS) {
+                return tl[idx - (F << j) + (1u << j)];
+            } else {
+                return ldg_tw(tab + idx);
+            }
+        };
         auto otf = [&](uint32_t idx) {
             // exponent of Psi[idx] is bitrev_logn(idx) = e = q*B + r
             const uint32_t e = __brev(idx) >> (32 - a.logn);
             return TwMul<true>{ldg_tw(ot + (e & (B_ot - 1u))), ldg_tw(ot + B_ot + (e >> a.ot_logb))};
         };
 
-        // global -> SMEM, 16-byte vectors, coalesced
+        // Round 0 touches e = o + k s with s = M >> r(0): when s >= 16 a warp's
+        // accesses are whole 128-byte segments, so the forward loads round 0
+        // straight from global and the inverse stores its last round (round 0)
+        // straight to global; the other end goes through SMEM with 16-byte
+        // vectors.
+        constexpr bool DIRECT0 = RoundGeo<LOGM, 0, LOGE>::s >= 16;
+        auto stage_in = [&]() {
 #pragma unroll
-        for (int j = 0; j < E / 2; ++j) {
-            const uint32_t ch = j * TB + tib;
-            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(g + 2 * ch);
-            *reinterpret_cast<ulonglong2*>(sb + swz(2 * ch)) = v;
-        }
-        block_sync<TB>(blk);
+            for (int j = 0; j < E / 2; ++j) {
+                const uint32_t ch = j * TB + tib;
+                const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(g + 2 * ch);
+                *reinterpret_cast<ulonglong2*>(sb + swz(2 * ch)) = v;
+            }
+            block_sync<TB>(blk);
+        };
+        auto stage_out = [&]() {
+            if (active) {
+#pragma unroll
+                for (int j = 0; j < E / 2; ++j) {
+                    const uint32_t ch = j * TB + tib;
+                    *reinterpret_cast<ulonglong2*>(g + 2 * ch) =
+                        *reinterpret_cast<const ulonglong2*>(sb + swz(2 * ch));
+                }
+            }
+            block_sync<TB>(blk);  // the next iteration reuses this SMEM block
+        };
 
         uint64_t x[16];
+        auto g_load0 = [&]() {
+            using Geo = RoundGeo<LOGM, 0, LOGE>;
+#pragma unroll
+            for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+                for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = g[Geo::elem(qd * TB + tib, k)];
+        };
+        auto g_store0 = [&]() {
+            using Geo = RoundGeo<LOGM, 0, LOGE>;
+            if (active) {
+#pragma unroll
+                for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+                    for (int k = 0; k < Geo::R; ++k) g[Geo::elem(qd * TB + tib, k)] = x[qd * Geo::R + k];
+            }
+        };
         // stride-1 rounds hold adjacent pairs (e, e+1): 128-bit SMEM accesses
         auto s_load = [&](auto ri) {
             using Geo = RoundGeo<LOGM, decltype(ri)::value, LOGE>;
@@ -221,19 +288,34 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE>::CT, ContigCfg<LOGM, LOG
             }
         };
 
+        auto tw_ready = [&]() {
+            if constexpr (TWS) {
+                cp_async_wait_all();
+                block_sync<TB>(blk);
+            }
+        };
         if constexpr (!INV) {
+            if constexpr (!DIRECT0) stage_in();
+            tw_ready();
             static_for<NR>([&](auto ri) {
                 constexpr int RI = decltype(ri)::value;
-                s_load(ri);
+                if constexpr (RI == 0 && DIRECT0) {
+                    g_load0();
+                } else {
+                    s_load(ri);
+                }
                 ct_round<LOGM, LOGE, RI, OT_FROM>(x, tib, F, tabf, otf, pc);
                 if constexpr (RI == NR - 1) {
 #pragma unroll
-                    for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // [0,8p) -> [0,p)
+                    for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // [0,8p+2^32) -> [0,p)
                 }
                 s_store(ri);
                 block_sync<TB>(blk);
             });
+            stage_out();
         } else {
+            stage_in();
+            tw_ready();
             static_for<NR>([&](auto rj) {
                 constexpr int RI = NR - 1 - decltype(rj)::value;
                 using RC = std::integral_constant<int, RI>;
@@ -243,20 +325,19 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE>::CT, ContigCfg<LOGM, LOG
 #pragma unroll
                     for (int k = 0; k < E; ++k) x[k] = norm4(x[k], pc);
                 }
-                s_store(RC{});
-                block_sync<TB>(blk);
+                if constexpr (RI == 0 && DIRECT0) {
+                    g_store0();
+                } else {
+                    s_store(RC{});
+                    block_sync<TB>(blk);
+                }
             });
-        }
-
-        // SMEM -> global
-        if (active) {
-#pragma unroll
-            for (int j = 0; j < E / 2; ++j) {
-                const uint32_t ch = j * TB + tib;
-                *reinterpret_cast<ulonglong2*>(g + 2 * ch) = *reinterpret_cast<const ulonglong2*>(sb + swz(2 * ch));
+            if constexpr (!DIRECT0) {
+                stage_out();
+            } else {
+                block_sync<TB>(blk);  // round-0 SMEM reads done before the next stage_in
             }
         }
-        block_sync<TB>(blk);
     }
 }
 
@@ -284,11 +365,11 @@ cudaError_t launch_cols_t(const KArgs& a, uint32_t rows, cudaStream_t st)
     return cudaPeekAtLastError();
 }
 
-template <int LOGM, int LOGE, bool INV, bool FUSE0, int OTS>
+template <int LOGM, int LOGE, bool INV, bool FUSE0, int OTS, bool TWS>
 cudaError_t launch_contig_t(KArgs a, uint32_t iters, cudaStream_t st)
 {
-    using CC = ContigCfg<LOGM, LOGE>;
-    auto fn = k_contig<LOGM, LOGE, INV, FUSE0, OTS>;
+    using CC = ContigCfg<LOGM, LOGE, TWS>;
+    auto fn = k_contig<LOGM, LOGE, INV, FUSE0, OTS, TWS>;
     static std::atomic<uint64_t> attr_set{0};  // one bit per device
     if (!set_once(attr_set)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
     a.iters = iters;
@@ -298,22 +379,22 @@ cudaError_t launch_contig_t(KArgs a, uint32_t iters, cudaStream_t st)
     return cudaPeekAtLastError();
 }
 
-template <int LOGM, int LOGE, bool INV, bool FUSE0>
+template <int LOGM, int LOGE, bool INV, bool FUSE0, bool TWS>
 cudaError_t launch_contig_ot(const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
 {
     switch (ots) {
-        case 0: return launch_contig_t<LOGM, LOGE, INV, FUSE0, 0>(a, iters, st);
-        case 1: return launch_contig_t<LOGM, LOGE, INV, FUSE0, 1>(a, iters, st);
-        default: return launch_contig_t<LOGM, LOGE, INV, FUSE0, (LOGM >= 2 ? 2 : LOGM)>(a, iters, st);
+        case 0: return launch_contig_t<LOGM, LOGE, INV, FUSE0, 0, TWS>(a, iters, st);
+        case 1: return launch_contig_t<LOGM, LOGE, INV, FUSE0, 1, TWS>(a, iters, st);
+        default: return launch_contig_t<LOGM, LOGE, INV, FUSE0, (LOGM >= 2 ? 2 : LOGM), TWS>(a, iters, st);
     }
 }
 
-template <int LOGE, bool INV, bool FUSE0, int... Ls>
+template <int LOGE, bool INV, bool FUSE0, bool TWS, int... Ls>
 cudaError_t contig_switch(int logm, const KArgs& a, int ots, uint32_t iters, cudaStream_t st,
                           std::integer_sequence<int, Ls...>)
 {
     cudaError_t err = cudaErrorInvalidValue;
-    ((logm == Ls ? (err = launch_contig_ot<Ls, LOGE, INV, FUSE0>(a, ots, iters, st), 0) : 0), ...);
+    ((logm == Ls ? (err = launch_contig_ot<Ls, LOGE, INV, FUSE0, TWS>(a, ots, iters, st), 0) : 0), ...);
     return err;
 }
 
@@ -339,18 +420,18 @@ using K1Pairs = std::integer_sequence<int, K1P(14, 6), K1P(14, 7), K1P(14, 8), K
 
 cudaError_t launch_single(bool inverse, const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
 {
-    return inverse ? contig_switch<4, true, true>((int)a.logn, a, ots, iters, st, SingleSizes{})
-                   : contig_switch<4, false, false>((int)a.logn, a, ots, iters, st, SingleSizes{});
+    return inverse ? contig_switch<4, true, true, false>((int)a.logn, a, ots, iters, st, SingleSizes{})
+                   : contig_switch<4, false, false, false>((int)a.logn, a, ots, iters, st, SingleSizes{});
 }
 
 cudaError_t launch_k2(bool inverse, int loge, const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
 {
     const int logm = (int)(a.logn - a.log_n1);
     if (loge == 3)
-        return inverse ? contig_switch<3, true, false>(logm, a, ots, iters, st, K2Sizes{})
-                       : contig_switch<3, false, false>(logm, a, ots, iters, st, K2Sizes{});
-    return inverse ? contig_switch<4, true, false>(logm, a, ots, iters, st, K2Sizes{})
-                   : contig_switch<4, false, false>(logm, a, ots, iters, st, K2Sizes{});
+        return inverse ? contig_switch<3, true, false, true>(logm, a, ots, iters, st, K2Sizes{})
+                       : contig_switch<3, false, false, true>(logm, a, ots, iters, st, K2Sizes{});
+    return inverse ? contig_switch<4, true, false, true>(logm, a, ots, iters, st, K2Sizes{})
+                   : contig_switch<4, false, false, true>(logm, a, ots, iters, st, K2Sizes{});
 }
 
 cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st)

@@ -146,6 +146,81 @@ __device__ __forceinline__ uint64_t shoup_ptx(uint64_t b, uint64_t w, uint64_t w
       "}" : "=l"(r) : "l"(b), "l"(w), "l"(wb), "l"(np));
   return r;
 }
+// V4: the kernels' PTX Shoup (re-paired); V5: FP64-assisted truncated quotient:
+// hi(b1 v0) + hi(b0 v1) ~ floor((b1 v0 + b0 v1) / 2^32) computed on the FP64
+// pipe with round-down (exact int->double via the 2^52 bias trick).
+__device__ __forceinline__ uint64_t shoup_v4(uint64_t b, uint64_t w, uint64_t wb, uint64_t np) {
+  uint64_t r;
+  asm("{\n\t.reg .u32 b0, b1, v0, v1, w0, w1, n0, n1, t0, t1, q0, q1, r0, r1;\n\t.reg .u64 q, a;\n\t"
+      "mov.b64 {b0, b1}, %1;\n\tmov.b64 {w0, w1}, %2;\n\tmov.b64 {v0, v1}, %3;\n\tmov.b64 {n0, n1}, %4;\n\t"
+      "mul.hi.u32 t0, b1, v0;\n\tmul.hi.u32 t1, b0, v1;\n\tmul.wide.u32 q, b1, v1;\n\tmov.b64 {q0, q1}, q;\n\t"
+      "add.cc.u32 q0, q0, t0;\n\taddc.u32 q1, q1, 0;\n\tadd.cc.u32 q0, q0, t1;\n\taddc.u32 q1, q1, 0;\n\t"
+      "mul.wide.u32 a, b0, w0;\n\tmad.wide.u32 a, q0, n0, a;\n\tmov.b64 {r0, r1}, a;\n\t"
+      "mad.lo.u32 r1, b0, w1, r1;\n\tmad.lo.u32 r1, b1, w0, r1;\n\tmad.lo.u32 r1, q0, n1, r1;\n\tmad.lo.u32 r1, q1, n0, r1;\n\t"
+      "mov.b64 %0, {r0, r1};\n\t}" : "=l"(r) : "l"(b), "l"(w), "l"(wb), "l"(np));
+  return r;
+}
+__device__ __forceinline__ uint64_t shoup_f64(uint64_t b, uint64_t w, uint64_t wb, uint64_t np, double V0, double V1) {
+  const uint32_t b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+  const double two52 = 4503599627370496.0;
+  const double B0 = __longlong_as_double((long long)(0x4330000000000000ull | b0)) - two52;
+  const double B1 = __longlong_as_double((long long)(0x4330000000000000ull | b1)) - two52;
+  const double t = __fma_rd(B1, V0, __dmul_rd(B0, V1));
+  const double u = __fma_rd(t, 2.3283064365386963e-10, two52);  // 2^52 + floor(t / 2^32)
+  const uint32_t c = (uint32_t)__double_as_longlong(u);
+  const uint64_t q = (uint64_t)b1 * (uint32_t)(wb >> 32) + c;
+  const uint32_t q0 = (uint32_t)q, q1 = (uint32_t)(q >> 32);
+  const uint32_t w0 = (uint32_t)w, w1 = (uint32_t)(w >> 32), n0 = (uint32_t)np, n1 = (uint32_t)(np >> 32);
+  uint64_t a = (uint64_t)b0 * w0 + (uint64_t)q0 * n0;
+  uint32_t hi = (uint32_t)(a >> 32) + b0 * w1 + b1 * w0 + q0 * n1 + q1 * n0;
+  return ((uint64_t)hi << 32) | (uint32_t)a;
+}
+__device__ __forceinline__ uint64_t shoup_f64b(uint64_t b, uint64_t w, uint64_t wb, uint64_t np, double V0, double V1) {
+  const uint32_t b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+  const double B0 = __uint2double_rn(b0), B1 = __uint2double_rn(b1);
+  const double t = __fma_rd(B1, V0, __dmul_rd(B0, V1));
+  const double u = __fma_rd(t, 2.3283064365386963e-10, 4503599627370496.0);
+  const uint32_t c = (uint32_t)__double_as_longlong(u);
+  const uint64_t q = (uint64_t)b1 * (uint32_t)(wb >> 32) + c;
+  const uint32_t q0 = (uint32_t)q, q1 = (uint32_t)(q >> 32);
+  const uint32_t w0 = (uint32_t)w, w1 = (uint32_t)(w >> 32), n0 = (uint32_t)np, n1 = (uint32_t)(np >> 32);
+  uint64_t a = (uint64_t)b0 * w0 + (uint64_t)q0 * n0;
+  uint32_t hi = (uint32_t)(a >> 32) + b0 * w1 + b1 * w0 + q0 * n1 + q1 * n0;
+  return ((uint64_t)hi << 32) | (uint32_t)a;
+}
+__device__ __forceinline__ uint64_t csub_hi(uint64_t x, uint64_t m, uint32_t mh) {
+  return (uint32_t)(x >> 32) > mh ? x - m : x;
+}
+template <int V>
+__global__ void k_bfw(uint64_t* out, uint64_t p, uint64_t w, uint64_t wb) {
+  uint64_t X[CH], Y[CH];
+  for (int c = 0; c < CH; ++c) { X[c] = (threadIdx.x * 77 + c) % p; Y[c] = (threadIdx.x * 31 + c * 5) % p; }
+  const uint64_t p5 = 5 * p, np = 0 - p;
+  const uint32_t p5h = (uint32_t)(p5 >> 32);
+  const double V0 = (double)(uint32_t)wb, V1 = (double)(uint32_t)(wb >> 32);
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      uint64_t x = csub_hi(X[c], p5, p5h);
+      uint64_t t = V == 4 ? shoup_v4(Y[c], w, wb, np) : V == 5 ? shoup_f64(Y[c], w, wb, np, V0, V1) : shoup_f64b(Y[c], w, wb, np, V0, V1);
+      X[c] = x + t; Y[c] = x - t + p5;
+    }
+  uint64_t s = 0;
+  for (int c = 0; c < CH; ++c) s ^= X[c] ^ Y[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+// correctness of the FP64 quotient variant against exact arithmetic (host check)
+__global__ void k_f64check(uint64_t* bad, const uint64_t* bs, uint64_t p, uint64_t w, uint64_t wb, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double V0 = (double)(uint32_t)wb, V1 = (double)(uint32_t)(wb >> 32);
+  uint64_t b = bs[i];
+  uint64_t r = shoup_f64(b, w, wb, 0 - p, V0, V1);
+  unsigned __int128 prod = (unsigned __int128)b * w;
+  uint64_t ex = (uint64_t)(prod % p);
+  if (r >= 5 * p || (r % p) != ex) atomicAdd((unsigned long long*)bad, 1ull);
+}
+
 template <int V>
 __global__ void k_bfv(uint64_t* out, uint64_t p, uint64_t w, uint64_t wb) {
   uint64_t X[CH], Y[CH];
@@ -240,6 +315,36 @@ int main() {
     double ops = (double)blocks * threads * ITERS * CH;
     printf("{\"kernel\": \"%s\", \"ms\": %.4f, \"Gops_per_s\": %.1f, \"ops_per_ns_per_sm\": %.3f}\n", k.name, ms,
            ops / ms / 1e6, ops / ms / 1e6 / sms);
+  }
+  {
+    for (int rep = 0; rep < 2; ++rep) k_bfw<4><<<blocks, threads>>>(out, p, w, wb);
+    for (int v = 4; v <= 6; ++v) {
+      if (v == 6) k_bfw<6><<<blocks, threads>>>(out, p, w, wb);
+      cudaEventRecord(e0);
+      if (v == 4) k_bfw<4><<<blocks, threads>>>(out, p, w, wb);
+      else if (v == 5) k_bfw<5><<<blocks, threads>>>(out, p, w, wb);
+      else k_bfw<6><<<blocks, threads>>>(out, p, w, wb);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      double ops = (double)blocks * threads * ITERS * CH;
+      printf("{\"kernel\": \"ct_w%d\", \"Gops_per_s\": %.1f}\n", v, ops / ms / 1e6);
+    }
+    // FP64 quotient correctness on random 64-bit inputs
+    const int n = 1 << 22;
+    uint64_t *bs, *bad;
+    cudaMalloc(&bs, n * 8);
+    cudaMalloc(&bad, 8);
+    cudaMemset(bad, 0, 8);
+    uint64_t* hb = (uint64_t*)malloc(n * 8);
+    uint64_t z = 12345;
+    for (int i = 0; i < n; ++i) { z ^= z << 13; z ^= z >> 7; z ^= z << 17; hb[i] = i < 64 ? ~(uint64_t)i : z; }
+    cudaMemcpy(bs, hb, n * 8, cudaMemcpyHostToDevice);
+    k_f64check<<<n / 256, 256>>>(bad, bs, p, w, wb, n);
+    uint64_t nb = 0;
+    cudaMemcpy(&nb, bad, 8, cudaMemcpyDeviceToHost);
+    printf("{\"check\": \"shoup_f64\", \"n\": %d, \"bad\": %llu}\n", n, (unsigned long long)nb);
   }
   // occupancy sweep for the PTX butterfly: warps per SM vs rate
   for (int wps : {4, 8, 12, 16, 24, 32, 48, 64}) {
