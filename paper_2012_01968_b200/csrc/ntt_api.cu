@@ -26,6 +26,8 @@ struct ntt_plan_s {
     std::vector<uint64_t> primes, psis;
     Tw* d_fwd = nullptr;  // [L][N]
     Tw* d_inv = nullptr;  // [L][N]
+    Tw* d_fwd2 = nullptr;  // [L][N] Kernel-2 order (K2Layout), two-kernel plans only
+    Tw* d_inv2 = nullptr;
     Tw* d_ot_fwd = nullptr;  // [L][B + N/B]
     Tw* d_ot_inv = nullptr;
     PrimeConst* d_pc = nullptr;  // [L]
@@ -60,6 +62,29 @@ unsigned default_log_n1(unsigned logn)
     }
 }
 
+// Kernel-2 twiddle order (ntt::K2Layout, runtime form): block bb of a row owns
+// N2 entries; round (S, r) stores Psi[(((F << S) + g) << i) + h] at
+// off(S) + ((2^i - 1 + h) << S) + g, F = N1 + bb.
+void build_k2_table(const Tw* std_tab, unsigned logn, unsigned log_n1, unsigned loge, Tw* out)
+{
+    const unsigned logm = logn - log_n1, le = std::min(loge, logm);
+    const uint32_t N1 = 1u << log_n1, N2 = 1u << logm;
+    for (uint32_t bb = 0; bb < N1; ++bb) {
+        const uint32_t F = N1 + bb;
+        Tw* o = out + (uint64_t)bb * N2;
+        o[0] = Tw{0, 0};
+        uint32_t off = 1;
+        for (unsigned S = 0; S < logm; S += le) {
+            const unsigned r = std::min(le, logm - S);
+            for (unsigned i = 0; i < r; ++i)
+                for (uint32_t h = 0; h < (1u << i); ++h)
+                    for (uint32_t g = 0; g < (1u << S); ++g)
+                        o[off + ((((1u << i) - 1u + h) << S) + g)] = std_tab[((((uint64_t)F << S) + g) << i) + h];
+            off += ((1u << r) - 1u) << S;
+        }
+    }
+}
+
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev)
@@ -82,6 +107,9 @@ void free_plan_memory(ntt_plan_s* p)
     cudaFree(p->d_ot_fwd);
     cudaFree(p->d_ot_inv);
     cudaFree(p->d_pc);
+    cudaFree(p->d_fwd2);
+    cudaFree(p->d_inv2);
+    p->d_fwd2 = p->d_inv2 = nullptr;
     p->d_fwd = p->d_inv = p->d_ot_fwd = p->d_ot_inv = nullptr;
     p->d_pc = nullptr;
 }
@@ -105,6 +133,7 @@ KArgs base_args(const ntt_plan_s* plan, uint64_t* data, unsigned batch, bool inv
     KArgs a{};
     a.data = data;
     a.tab = inverse ? plan->d_inv : plan->d_fwd;
+    a.tab2 = inverse ? plan->d_inv2 : plan->d_fwd2;
     a.ot = inverse ? plan->d_ot_inv : plan->d_ot_fwd;
     a.pc = plan->d_pc;
     a.L = plan->L;
@@ -260,7 +289,7 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
     // tuning knob (experiments only): NTT_LOGE="k1,k2" per-thread radix exponents
     if (const char* v = std::getenv("NTT_LOGE")) {
         int a1 = 4, a2 = 4;
-        if (std::sscanf(v, "%d,%d", &a1, &a2) == 2 && (a1 == 3 || a1 == 4) && (a2 == 3 || a2 == 4)) {
+        if (std::sscanf(v, "%d,%d", &a1, &a2) == 2 && (a1 == 3 || a1 == 4) && (a2 >= 3 && a2 <= 6)) {
             p->loge_k1 = a1;
             p->loge_k2 = a2;
         }
@@ -302,10 +331,29 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
         });
     for (auto& t : th) t.join();
 
+    // Kernel-2 ordered copies for the two-kernel path
+    const bool k2tab = log_n1 != 0;
+    std::vector<Tw> h_fwd2, h_inv2;
+    if (k2tab) {
+        const unsigned loge = (p->loge_k2 == 3 || p->loge_k2 == 6) ? 3 : 4;
+        h_fwd2.resize(N * L);
+        h_inv2.resize(N * L);
+        std::vector<std::thread> th2;
+        for (unsigned t = 0; t < nth; ++t)
+            th2.emplace_back([&, t] {
+                for (unsigned l = t; l < L; l += nth) {
+                    build_k2_table(&h_fwd[l * N], logn, log_n1, loge, &h_fwd2[l * N]);
+                    build_k2_table(&h_inv[l * N], logn, log_n1, loge, &h_inv2[l * N]);
+                }
+            });
+        for (auto& t : th2) t.join();
+    }
+
     const size_t bt = sizeof(Tw) * N * L, bo = sizeof(Tw) * NOT * L, bp = sizeof(PrimeConst) * L;
     if (cudaMalloc(&p->d_fwd, bt) != cudaSuccess || cudaMalloc(&p->d_inv, bt) != cudaSuccess ||
         cudaMalloc(&p->d_ot_fwd, bo) != cudaSuccess || cudaMalloc(&p->d_ot_inv, bo) != cudaSuccess ||
-        cudaMalloc(&p->d_pc, bp) != cudaSuccess) {
+        cudaMalloc(&p->d_pc, bp) != cudaSuccess ||
+        (k2tab && (cudaMalloc(&p->d_fwd2, bt) != cudaSuccess || cudaMalloc(&p->d_inv2, bt) != cudaSuccess))) {
         cudaGetLastError();
         free_plan_memory(p);
         delete p;
@@ -315,13 +363,15 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
         cudaMemcpy(p->d_inv, h_inv.data(), bt, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(p->d_ot_fwd, h_otf.data(), bo, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(p->d_ot_inv, h_oti.data(), bo, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(p->d_pc, h_pc.data(), bp, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaMemcpy(p->d_pc, h_pc.data(), bp, cudaMemcpyHostToDevice) != cudaSuccess ||
+        (k2tab && (cudaMemcpy(p->d_fwd2, h_fwd2.data(), bt, cudaMemcpyHostToDevice) != cudaSuccess ||
+                   cudaMemcpy(p->d_inv2, h_inv2.data(), bt, cudaMemcpyHostToDevice) != cudaSuccess))) {
         cudaGetLastError();
         free_plan_memory(p);
         delete p;
         return NTT_ERR_CUDA;
     }
-    p->table_bytes = 2 * bt + 2 * bo + bp;
+    p->table_bytes = (k2tab ? 4 : 2) * bt + 2 * bo + bp;
     *out = p;
     return NTT_OK;
 }

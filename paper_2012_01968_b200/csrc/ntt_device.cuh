@@ -30,6 +30,7 @@ struct __align__(16) PrimeConst {
 struct KArgs {
     uint64_t* data;        // [batch][L][N]
     const Tw* tab;         // [L][N] Psi (forward) or Psi^-1 (inverse)
+    const Tw* tab2;        // [L][N1][N2] the same twiddles in Kernel-2 order (K2Layout)
     const Tw* ot;          // [L][B + N/B] OT bases (fine | coarse), forward or inverse
     const PrimeConst* pc;  // [L]
     uint32_t L, batch;
@@ -196,12 +197,41 @@ struct RoundGeo {
     }
 };
 
+// Kernel-2 twiddle layout.  Block bb (F = N1 + bb) owns N2 entries; round ri
+// (stages [S, S+r)) holds, at round_off(S) + ((2^i - 1 + h) << S) + g, the
+// twiddle Psi[(((F << S) + g) << i) + h] of stage S+i, twiddle h, group g.
+// Entry 0 is padding.  Host and device share this definition.
+template <int LOGM, int LOGE>
+struct K2Layout {
+    static constexpr int LE = LOGM < LOGE ? LOGM : LOGE;
+    __host__ __device__ static constexpr uint32_t round_off(int S)
+    {
+        uint32_t off = 1;
+        for (int s0 = 0; s0 < S; s0 += LE) {
+            const int r = (LOGM - s0) < LE ? (LOGM - s0) : LE;
+            off += ((1u << r) - 1u) << s0;
+        }
+        return off;
+    }
+};
+
 // Forward round: r Cooley-Tukey stages on each of the thread's GPT groups.
-// tabf(idx, j) returns the table twiddle Psi[idx] of local stage j; otf(idx)
-// the OT factor pair.
+// Twiddle indices are formed for F = 1 ("local" index: the block's own
+// sub-table, tl[2^j + h] = Psi[F 2^j + h]); Fm1 = F - 1 shifts them to the
+// global index idx + (Fm1 << j) where a global table or OT needs it.
+// tabf(TwKey) returns the twiddle (the key carries both the local index and
+// its (stage, h, group) coordinates, for tables laid out per round);
+// otf(idx_global) the OT factor pair.
 // OT_FROM = first local stage whose twiddles come from OT (>= LOGM: none).
+struct TwKey {
+    uint32_t idx;  // local index ((1 << S) + g) << i) + h
+    int j;         // local stage S + i
+    int S, i, h;   // round start, stage within round, twiddle within stage
+    uint32_t g;    // group
+};
+
 template <int LOGM, int LOGE, int RI, int OT_FROM, class TabF, class OtF>
-__device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32_t F, const TabF& tabf,
+__device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
                                          const OtF& otf, const PrimeConst& c)
 {
     using Geo = RoundGeo<LOGM, RI, LOGE>;
@@ -209,7 +239,7 @@ __device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32
 #pragma unroll
     for (int qd = 0; qd < Geo::GPT; ++qd) {
         const uint32_t G = qd * Geo::TB + tib;
-        const uint32_t B = (F << S) + G / Geo::s;
+        const uint32_t B = (1u << S) + G / Geo::s;
 #pragma unroll
         for (int i = 0; i < Geo::r; ++i) {
             const int half = R >> (i + 1);
@@ -217,12 +247,12 @@ __device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32
             for (int h = 0; h < (1 << i); ++h) {
                 const uint32_t idx = (B << i) + h;
                 if (S + i >= OT_FROM) {
-                    const TwMul<true> w = otf(idx);
+                    const TwMul<true> w = otf(idx + (Fm1 << (S + i)));
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
                         ct_bf(x[qd * R + k], x[qd * R + k + half], w, c);
                 } else {
-                    const TwMul<false> w{tabf(idx, S + i)};
+                    const TwMul<false> w{tabf(TwKey{idx, S + i, S, i, h, G / Geo::s})};
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
                         ct_bf(x[qd * R + k], x[qd * R + k + half], w, c);
@@ -236,7 +266,7 @@ __device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32
 // in reverse order.  FUSE0: local stage 0 is global stage 0 (m = 1), where
 // N^-1 is fused: X' = (X+Y) N^-1, Y' = (X-Y) Psi^-1[1] N^-1 (R15).
 template <int LOGM, int LOGE, int RI, int OT_FROM, bool FUSE0, class TabF, class OtF>
-__device__ __forceinline__ void gs_round(uint64_t (&x)[16], uint32_t tib, uint32_t F, const TabF& tabf,
+__device__ __forceinline__ void gs_round(uint64_t (&x)[16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
                                          const OtF& otf, const PrimeConst& c)
 {
     using Geo = RoundGeo<LOGM, RI, LOGE>;
@@ -244,7 +274,7 @@ __device__ __forceinline__ void gs_round(uint64_t (&x)[16], uint32_t tib, uint32
 #pragma unroll
     for (int qd = 0; qd < Geo::GPT; ++qd) {
         const uint32_t G = qd * Geo::TB + tib;
-        const uint32_t B = (F << S) + G / Geo::s;
+        const uint32_t B = (1u << S) + G / Geo::s;
 #pragma unroll
         for (int i = Geo::r - 1; i >= 0; --i) {
             const int half = R >> (i + 1);
@@ -262,12 +292,12 @@ __device__ __forceinline__ void gs_round(uint64_t (&x)[16], uint32_t tib, uint32
             for (int h = 0; h < (1 << i); ++h) {
                 const uint32_t idx = (B << i) + h;
                 if (S + i >= OT_FROM) {
-                    const TwMul<true> w = otf(idx);
+                    const TwMul<true> w = otf(idx + (Fm1 << (S + i)));
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
                         gs_bf(x[qd * R + k], x[qd * R + k + half], w, c);
                 } else {
-                    const TwMul<false> w{tabf(idx, S + i)};
+                    const TwMul<false> w{tabf(TwKey{idx, S + i, S, i, h, G / Geo::s})};
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
                         gs_bf(x[qd * R + k], x[qd * R + k + half], w, c);

@@ -15,6 +15,7 @@
 #include "ntt_device.cuh"
 #include "ntt_launch.h"
 
+#include <algorithm>
 #include <atomic>
 
 namespace ntt {
@@ -47,7 +48,7 @@ __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>
 
     for (uint32_t i = tid; i < (uint32_t)M; i += CT) tws[i] = ldg_tw(tab + i);  // Psi[0..N1)
     __syncthreads();
-    auto tabf = [&](uint32_t idx, int) { return tws[idx]; };
+    auto tabf = [&](const TwKey& k) { return tws[k.idx]; };
     auto otf = [&](uint32_t) { return TwMul<true>{}; };  // OT never reaches Kernel-1
 
     uint64_t x[16];
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>
             } else {
                 s_load(ri);
             }
-            ct_round<LOGN1, LOGE, RI, 1 << 20>(x, tib, 1u, tabf, otf, pc);
+            ct_round<LOGN1, LOGE, RI, 1 << 20>(x, tib, 0u, tabf, otf, pc);
             if constexpr (RI == NR - 1) {
                 g_store(ri);  // [0, 8p): Kernel-2 continues the lazy chain
             } else {
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>
             } else {
                 s_load(RC{});
             }
-            gs_round<LOGN1, LOGE, RI, 1 << 20, true>(x, tib, 1u, tabf, otf, pc);
+            gs_round<LOGN1, LOGE, RI, 1 << 20, true>(x, tib, 0u, tabf, otf, pc);
             if constexpr (RI == 0) {
 #pragma unroll
                 for (int k = 0; k < SC::E; ++k) x[k] = norm4(x[k], pc);  // canonical [0, p)
@@ -128,7 +129,7 @@ struct ContigCfg {
     static constexpr int NB = CT / TB;              // blocks per CTA iteration
     // data words, plus (TWS) each block's local twiddle table of M entries
     static constexpr size_t SMEM = (size_t)NB * (1 << LOGM) * (8 + (TWS ? sizeof(Tw) : 0));
-    static constexpr int MINB = CT > 256 ? 1 : (LOGE >= 4 ? 2 : 3);  // register budget
+    static constexpr int MINB = CT > 256 ? 1 : (LOGE >= 4 ? 4 : 3);  // register budget
 };
 
 // 16-byte asynchronous global -> shared copy (LDGSTS), and its completion.
@@ -196,11 +197,11 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
                 }
             }
         }
-        auto tabf = [&](uint32_t idx, int j) {
+        auto tabf = [&](const TwKey& k) {
             if constexpr (TWS) {
-                return tl[idx - (F << j) + (1u << j)];
+                return tl[k.idx];
             } else {
-                return ldg_tw(tab + idx);
+                return ldg_tw(tab + k.idx + ((F - 1u) << k.j));
             }
         };
         auto otf = [&](uint32_t idx) {
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
                 } else {
                     s_load(ri);
                 }
-                ct_round<LOGM, LOGE, RI, OT_FROM>(x, tib, F, tabf, otf, pc);
+                ct_round<LOGM, LOGE, RI, OT_FROM>(x, tib, F - 1u, tabf, otf, pc);
                 if constexpr (RI == NR - 1) {
 #pragma unroll
                     for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // [0,8p+2^32) -> [0,p)
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
                 constexpr int RI = NR - 1 - decltype(rj)::value;
                 using RC = std::integral_constant<int, RI>;
                 s_load(RC{});
-                gs_round<LOGM, LOGE, RI, OT_FROM, FUSE0>(x, tib, F, tabf, otf, pc);
+                gs_round<LOGM, LOGE, RI, OT_FROM, FUSE0>(x, tib, F - 1u, tabf, otf, pc);
                 if constexpr (FUSE0 && RI == 0) {
 #pragma unroll
                     for (int k = 0; k < E; ++k) x[k] = norm4(x[k], pc);
@@ -339,6 +340,171 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
             }
         }
     }
+}
+
+// ---------------------------------------------------------------- Kernel-2, pipelined
+// Persistent Kernel-2 / Kernel-2': each group of TB threads ("slot") walks the
+// N2-blocks in a grid-stride loop, prime-major, and prefetches block i+1 into
+// the second half of a double buffer with cp.async (LDGSTS, swizzled
+// destination) while it transforms block i -- the load latency of one block
+// hides behind the arithmetic of the previous one.  Twiddles come through the
+// read-only path (the current prime's table stays L2-resident).
+// The block's twiddles (Kernel-2 layout: one contiguous N2-entry segment per
+// block) are prefetched with the data, so no global load sits on the
+// critical path of a round.  SMEM per slot: 2 x (8 + 16) x N2 bytes.
+template <int LOGM, int LOGE>
+struct PipeCfg {
+    static constexpr int TB = Sched<LOGM, LOGE>::TB;
+    static constexpr int NB = TB >= 64 ? 4 : 4;  // slots per CTA
+    static constexpr int CT = NB * TB;
+    static constexpr size_t SMEM = (size_t)2 * NB * (1 << LOGM) * (8 + sizeof(Tw));
+    static constexpr int MINB = LOGE >= 4 ? 2 : 3;
+};
+
+template <int LOGM, int LOGE, bool INV, int OTS>
+__global__ void __launch_bounds__(PipeCfg<LOGM, LOGE>::CT, PipeCfg<LOGM, LOGE>::MINB) k_blocks(const KArgs a)
+{
+    using SC = Sched<LOGM, LOGE>;
+    using PC = PipeCfg<LOGM, LOGE>;
+    constexpr int M = SC::M, E = SC::E, TB = SC::TB, NR = SC::NR, NB = PC::NB;
+    constexpr int OT_FROM = OTS ? LOGM - OTS : (1 << 20);
+    static_assert(TB <= 256 && NB >= 1, "block size");
+    extern __shared__ __align__(16) uint64_t sm[];
+
+    const uint32_t tid = threadIdx.x, blk = tid / TB, tib = tid % TB;
+    const uint32_t n1mask = (1u << a.log_n1) - 1u;
+    const uint32_t B_ot = 1u << a.ot_logb;
+    const uint32_t nslots = gridDim.x * NB;
+
+    auto block_ptr = [&](uint32_t gb, uint32_t& l, uint32_t& bb) {
+        bb = gb & n1mask;
+        const uint32_t q = gb >> a.log_n1;  // prime-major: q = l * batch + b
+        l = q / a.batch;
+        const uint32_t b = q - l * a.batch;
+        return a.data + (((uint64_t)b * a.L + l) << a.logn) + (uint64_t)bb * M;
+    };
+    Tw* const tw_base = reinterpret_cast<Tw*>(sm + 2 * NB * M);
+    auto prefetch = [&](uint32_t gb, uint32_t buf) {
+        if (gb < a.total_blocks) {
+            uint32_t l, bb;
+            const uint64_t* g = block_ptr(gb, l, bb);
+            uint64_t* sd = sm + (buf * NB + blk) * M;
+#pragma unroll
+            for (int j = 0; j < E / 2; ++j) {
+                const uint32_t ch = j * TB + tib;
+                cp_async16(sd + swz(2 * ch), g + 2 * ch);
+            }
+            const Tw* t2 = a.tab2 + ((uint64_t)l << a.logn) + ((uint64_t)bb << LOGM);
+            Tw* st = tw_base + (buf * NB + blk) * M;
+#pragma unroll
+            for (int j = 0; j < E; ++j) cp_async16(st + j * TB + tib, t2 + j * TB + tib);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    uint32_t gb = blockIdx.x * NB + blk;
+    prefetch(gb, 0);
+    for (uint32_t it = 0; gb < a.total_blocks; ++it, gb += nslots) {
+        uint64_t* sb = sm + ((it & 1) * NB + blk) * M;
+        const Tw* tws = tw_base + ((it & 1) * NB + blk) * M;
+        prefetch(gb + nslots, (it + 1) & 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        block_sync<TB>(blk);
+
+        uint32_t l, bb;
+        uint64_t* g = block_ptr(gb, l, bb);
+        const uint32_t Fm1 = (1u << a.log_n1) + bb - 1u;
+        const Tw* tab = a.tab + ((uint64_t)l << a.logn);
+        const Tw* ot = a.ot + (uint64_t)l * (B_ot + ((1u << a.logn) >> a.ot_logb));
+        const PrimeConst pc = a.pc[l];
+        // Kernel-2 table segment (plan-built, per block, per round, [i][h][g]),
+        // prefetched into SMEM: the lanes of a warp read consecutive groups g.
+        auto tabf = [&](const TwKey& k) {
+            return tws[K2Layout<LOGM, LOGE>::round_off(k.S) + ((((1u << k.i) - 1u + k.h) << k.S) + k.g)];
+        };
+        auto otf = [&](uint32_t idx) {
+            const uint32_t e = __brev(idx) >> (32 - a.logn);  // exponent of Psi[idx]
+            return TwMul<true>{ldg_tw(ot + (e & (B_ot - 1u))), ldg_tw(ot + B_ot + (e >> a.ot_logb))};
+        };
+
+        uint64_t x[16];
+        auto s_load = [&](auto ri) {
+            using Geo = RoundGeo<LOGM, decltype(ri)::value, LOGE>;
+#pragma unroll
+            for (int qd = 0; qd < Geo::GPT; ++qd) {
+                if constexpr (Geo::s == 1 && Geo::R >= 2) {
+#pragma unroll
+                    for (int k = 0; k < Geo::R; k += 2) {
+                        const ulonglong2 v =
+                            *reinterpret_cast<const ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k)));
+                        x[qd * Geo::R + k] = v.x;
+                        x[qd * Geo::R + k + 1] = v.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = sb[swz(Geo::elem(qd * TB + tib, k))];
+                }
+            }
+        };
+        auto s_store = [&](auto ri) {
+            using Geo = RoundGeo<LOGM, decltype(ri)::value, LOGE>;
+#pragma unroll
+            for (int qd = 0; qd < Geo::GPT; ++qd) {
+                if constexpr (Geo::s == 1 && Geo::R >= 2) {
+#pragma unroll
+                    for (int k = 0; k < Geo::R; k += 2)
+                        *reinterpret_cast<ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k))) =
+                            make_ulonglong2(x[qd * Geo::R + k], x[qd * Geo::R + k + 1]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < Geo::R; ++k) sb[swz(Geo::elem(qd * TB + tib, k))] = x[qd * Geo::R + k];
+                }
+            }
+        };
+        auto stage_out = [&]() {
+#pragma unroll
+            for (int j = 0; j < E / 2; ++j) {
+                const uint32_t ch = j * TB + tib;
+                *reinterpret_cast<ulonglong2*>(g + 2 * ch) = *reinterpret_cast<const ulonglong2*>(sb + swz(2 * ch));
+            }
+        };
+        constexpr bool DIRECT0 = RoundGeo<LOGM, 0, LOGE>::s >= 16;
+
+        if constexpr (!INV) {
+            static_for<NR>([&](auto ri) {
+                constexpr int RI = decltype(ri)::value;
+                s_load(ri);
+                ct_round<LOGM, LOGE, RI, OT_FROM>(x, tib, Fm1, tabf, otf, pc);
+                if constexpr (RI == NR - 1) {
+#pragma unroll
+                    for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // [0,8p+2^32) -> [0,p)
+                }
+                s_store(ri);
+                block_sync<TB>(blk);
+            });
+            stage_out();
+        } else {
+            static_for<NR>([&](auto rj) {
+                constexpr int RI = NR - 1 - decltype(rj)::value;
+                using RC = std::integral_constant<int, RI>;
+                s_load(RC{});
+                gs_round<LOGM, LOGE, RI, OT_FROM, false>(x, tib, Fm1, tabf, otf, pc);
+                if constexpr (RI == 0 && DIRECT0) {
+                    using Geo = RoundGeo<LOGM, 0, LOGE>;
+#pragma unroll
+                    for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+                        for (int k = 0; k < Geo::R; ++k) g[Geo::elem(qd * TB + tib, k)] = x[qd * Geo::R + k];
+                } else {
+                    s_store(RC{});
+                    block_sync<TB>(blk);
+                }
+            });
+            if constexpr (!DIRECT0) stage_out();
+        }
+        block_sync<TB>(blk);  // all reads of this buffer done before it is refilled
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // ---------------------------------------------------------------- dispatch
@@ -377,6 +543,44 @@ cudaError_t launch_contig_t(KArgs a, uint32_t iters, cudaStream_t st)
     const uint64_t grid = (a.total_blocks + per_cta - 1) / per_cta;
     fn<<<(unsigned)grid, CC::CT, CC::SMEM, st>>>(a);
     return cudaPeekAtLastError();
+}
+
+template <int LOGM, int LOGE, bool INV, int OTS>
+cudaError_t launch_blocks_t(KArgs a, cudaStream_t st)
+{
+    using PC = PipeCfg<LOGM, LOGE>;
+    auto fn = k_blocks<LOGM, LOGE, INV, OTS>;
+    static std::atomic<uint64_t> attr_set{0};  // one bit per device
+    static int ctas_per_sm = 0;
+    if (!set_once(attr_set)) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, fn, PC::CT, PC::SMEM);
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t want = ((uint64_t)a.total_blocks + PC::NB - 1) / PC::NB;
+    const uint64_t grid = std::min<uint64_t>(want, (uint64_t)sms * std::max(1, ctas_per_sm));
+    fn<<<(unsigned)grid, PC::CT, PC::SMEM, st>>>(a);
+    return cudaPeekAtLastError();
+}
+
+template <int LOGM, int LOGE, bool INV>
+cudaError_t launch_blocks_ot(const KArgs& a, int ots, cudaStream_t st)
+{
+    switch (ots) {
+        case 0: return launch_blocks_t<LOGM, LOGE, INV, 0>(a, st);
+        case 1: return launch_blocks_t<LOGM, LOGE, INV, 1>(a, st);
+        default: return launch_blocks_t<LOGM, LOGE, INV, 2>(a, st);
+    }
+}
+
+template <int LOGE, bool INV, int... Ls>
+cudaError_t blocks_switch(int logm, const KArgs& a, int ots, cudaStream_t st, std::integer_sequence<int, Ls...>)
+{
+    cudaError_t err = cudaErrorInvalidValue;
+    ((logm == Ls ? (err = launch_blocks_ot<Ls, LOGE, INV>(a, ots, st), 0) : 0), ...);
+    return err;
 }
 
 template <int LOGM, int LOGE, bool INV, bool FUSE0, bool TWS>
@@ -427,6 +631,12 @@ cudaError_t launch_single(bool inverse, const KArgs& a, int ots, uint32_t iters,
 cudaError_t launch_k2(bool inverse, int loge, const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
 {
     const int logm = (int)(a.logn - a.log_n1);
+    if (loge == 5)  // pipelined persistent Kernel-2 (radix 16)
+        return inverse ? blocks_switch<4, true>(logm, a, ots, st, K2Sizes{})
+                       : blocks_switch<4, false>(logm, a, ots, st, K2Sizes{});
+    if (loge == 6)  // pipelined persistent Kernel-2 (radix 8)
+        return inverse ? blocks_switch<3, true>(logm, a, ots, st, K2Sizes{})
+                       : blocks_switch<3, false>(logm, a, ots, st, K2Sizes{});
     if (loge == 3)
         return inverse ? contig_switch<3, true, false, true>(logm, a, ots, iters, st, K2Sizes{})
                        : contig_switch<3, false, false, true>(logm, a, ots, iters, st, K2Sizes{});

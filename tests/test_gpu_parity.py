@@ -216,3 +216,13 @@ def test_full_size_configs(name, ot):
     del want
     plan.inverse(d)
     assert np.array_equal(to_host(d), x)
+
+
+@pytest.mark.parametrize("variant", ["4,3", "4,5", "4,6"])
+@pytest.mark.parametrize("logn,log_n1", [(14, 7), (15, 7), (16, 8), (17, 8), (17, 7), (17, 9)])
+def test_kernel2_variants(variant, logn, log_n1, monkeypatch):
+    """Kernel-2 implementations (radix 8 / 16, one-shot / pipelined persistent)
+    selected with the NTT_LOGE tuning knob: all bit-exact, OT on and off."""
+    monkeypatch.setenv("NTT_LOGE", variant)
+    check_roundtrip(1 << logn, 3, 2, log_n1=log_n1)
+    check_roundtrip(1 << logn, 2, 1, log_n1=log_n1, ot=True)
