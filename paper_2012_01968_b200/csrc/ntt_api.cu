@@ -32,7 +32,7 @@ struct ntt_plan_s {
     Tw* d_ot_inv = nullptr;
     PrimeConst* d_pc = nullptr;  // [L]
     uint64_t table_bytes = 0;
-    int loge_k1 = 4, loge_k2 = 4;  // per-thread radix of Kernel-1 / Kernel-2
+    int loge_k1 = 4, loge_k2 = 5;  // Kernel-1 radix exponent; Kernel-2 variant (5 = pipelined radix-16)
 };
 
 namespace {
@@ -288,7 +288,7 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
     p->psis.assign(L, 0);
     // tuning knob (experiments only): NTT_LOGE="k1,k2" per-thread radix exponents
     if (const char* v = std::getenv("NTT_LOGE")) {
-        int a1 = 4, a2 = 4;
+        int a1 = 4, a2 = 5;
         if (std::sscanf(v, "%d,%d", &a1, &a2) == 2 && (a1 == 3 || a1 == 4) && (a2 >= 3 && a2 <= 6)) {
             p->loge_k1 = a1;
             p->loge_k2 = a2;
@@ -322,7 +322,7 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
                 c.np = 0 - q;
                 c.p5 = 5 * q;
                 c.p4_hi = (uint32_t)((4 * q) >> 32);
-                c.pad = 0;
+                c.rn = (uint32_t)((((unsigned __int128)1) << 90) / q);
                 nttp::Twiddle t1 = nttp::shoup_pair(ninv, q), t2 = nttp::shoup_pair(ninv_psi, q);
                 c.ninv = Tw{t1.w, t1.wb};
                 c.ninv_psi = Tw{t2.w, t2.wb};

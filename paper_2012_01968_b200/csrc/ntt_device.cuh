@@ -21,7 +21,8 @@ struct __align__(16) PrimeConst {
     uint64_t p, p2, p4;  // p, 2p, 4p
     uint64_t np;         // 2^64 - p
     uint64_t p5;         // 5p: the GS difference offset (section 5.1)
-    uint32_t p4_hi, pad;  // high word of 4p
+    uint32_t p4_hi;      // high word of 4p
+    uint32_t rn;         // floor(2^90 / p): quotient estimate for the final reduction
     Tw ninv;             // N^-1
     Tw ninv_psi;         // N^-1 * Psi^-1[1], the fused last GS stage (R15)
 };
@@ -307,15 +308,21 @@ __device__ __forceinline__ void gs_round(uint64_t (&x)[16], uint32_t tib, uint32
     }
 }
 
-// Canonical reductions at the end of a direction.
-__device__ __forceinline__ uint64_t norm8(uint64_t x, const PrimeConst& c)  // [0,8p+2^32) -> [0,p)
+// Canonical reduction at the end of a direction, for any x < 2^64:
+//   q = floor(hi(x) * rn / 2^58),  rn = floor(2^90 / p) < 2^32 (p > 2^59),
+// satisfies floor(x/p) - 1 <= q <= floor(x/p) (the dropped low word and the
+// floor of rn each cost < 2^-26 of a unit), so x - q p lies in [0, 2p) and
+// one exact conditional subtraction finishes: 1 IMAD.HI + 1 IMAD.WIDE +
+// 1 IMAD instead of a chain of three or four conditional subtractions.
+__device__ __forceinline__ uint64_t reduce_full(uint64_t x, const PrimeConst& c)
 {
-    return csub(csub(csub(csub(x, c.p4), c.p2), c.p), c.p);
+    const uint32_t q = __umulhi((uint32_t)(x >> 32), c.rn) >> 26;
+    return csub(x - (uint64_t)q * c.p, c.p);
 }
-__device__ __forceinline__ uint64_t norm4(uint64_t x, const PrimeConst& c)  // [0,4p) -> [0,p)
-{
-    return csub(csub(x, c.p2), c.p);
-}
+__device__ __forceinline__ uint64_t norm8(uint64_t x, const PrimeConst& c) { return reduce_full(x, c); }
+// [0,4p) -> [0,p) (inverse outputs): two exact conditional subtractions, all
+// on the ALU pipe -- cheaper than reduce_full where the multiply pipe binds.
+__device__ __forceinline__ uint64_t norm4(uint64_t x, const PrimeConst& c) { return csub(csub(x, c.p2), c.p); }
 
 // SMEM swizzle for contiguous blocks: XOR word-address bits 1..3 with
 // (bits 4..6 ^ bits 5..7).  16-byte pairs (2i, 2i+1) stay adjacent (vector

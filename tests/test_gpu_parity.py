@@ -218,7 +218,14 @@ def test_full_size_configs(name, ot):
     assert np.array_equal(to_host(d), x)
 
 
-@pytest.mark.parametrize("variant", ["4,3", "4,5", "4,6"])
+@pytest.mark.parametrize("L", [1, 2, 7, 16, 45])
+def test_c5_prime_sweep(L):
+    """BASELINE.json C5 (mixed stream): N=2^16, one ciphertext per request,
+    L swept over 1..45 -- every L in the two-kernel path."""
+    check_roundtrip(1 << 16, L, 1)
+
+
+@pytest.mark.parametrize("variant", ["4,3", "4,4", "4,5", "4,6"])
 @pytest.mark.parametrize("logn,log_n1", [(14, 7), (15, 7), (16, 8), (17, 8), (17, 7), (17, 9)])
 def test_kernel2_variants(variant, logn, log_n1, monkeypatch):
     """Kernel-2 implementations (radix 8 / 16, one-shot / pipelined persistent)
