@@ -289,7 +289,7 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
     // tuning knob (experiments only): NTT_LOGE="k1,k2" per-thread radix exponents
     if (const char* v = std::getenv("NTT_LOGE")) {
         int a1 = 4, a2 = 5;
-        if (std::sscanf(v, "%d,%d", &a1, &a2) == 2 && (a1 == 3 || a1 == 4) && (a2 >= 3 && a2 <= 6)) {
+        if (std::sscanf(v, "%d,%d", &a1, &a2) == 2 && (a1 >= 3 && a1 <= 5) && (a2 >= 3 && a2 <= 6)) {
             p->loge_k1 = a1;
             p->loge_k2 = a2;
         }

@@ -20,6 +20,14 @@
 
 namespace ntt {
 
+// 16-byte asynchronous global -> shared copy (LDGSTS), and its completion.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
+{
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ---------------------------------------------------------------- Kernel-1
 template <int LOGN1, int LOGE>
 struct ColsCfg {
@@ -52,35 +60,42 @@ __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>
     auto otf = [&](uint32_t) { return TwMul<true>{}; };  // OT never reaches Kernel-1
 
     uint64_t x[16];
+    // element e_k = e_0 + k s: one base address per group, compile-time offsets for k
     auto g_load = [&](auto ri) {
         using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
 #pragma unroll
-        for (int qd = 0; qd < Geo::GPT; ++qd)
+        for (int qd = 0; qd < Geo::GPT; ++qd) {
+            const uint64_t* p = col + ((uint64_t)Geo::elem(qd * SC::TB + tib, 0) << logn2);
 #pragma unroll
-            for (int k = 0; k < Geo::R; ++k)
-                x[qd * Geo::R + k] = col[(uint64_t)Geo::elem(qd * SC::TB + tib, k) << logn2];
+            for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = p[(size_t)(k * Geo::s) << logn2];
+        }
     };
     auto g_store = [&](auto ri) {
         using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
 #pragma unroll
-        for (int qd = 0; qd < Geo::GPT; ++qd)
+        for (int qd = 0; qd < Geo::GPT; ++qd) {
+            uint64_t* p = col + ((uint64_t)Geo::elem(qd * SC::TB + tib, 0) << logn2);
 #pragma unroll
-            for (int k = 0; k < Geo::R; ++k)
-                col[(uint64_t)Geo::elem(qd * SC::TB + tib, k) << logn2] = x[qd * Geo::R + k];
+            for (int k = 0; k < Geo::R; ++k) p[(size_t)(k * Geo::s) << logn2] = x[qd * Geo::R + k];
+        }
     };
     auto s_load = [&](auto ri) {
         using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
 #pragma unroll
-        for (int qd = 0; qd < Geo::GPT; ++qd)
+        for (int qd = 0; qd < Geo::GPT; ++qd) {
+            const uint64_t* p = sm + Geo::elem(qd * SC::TB + tib, 0) * 16 + c;
 #pragma unroll
-            for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = sm[Geo::elem(qd * SC::TB + tib, k) * 16 + c];
+            for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = p[k * Geo::s * 16];
+        }
     };
     auto s_store = [&](auto ri) {
         using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
 #pragma unroll
-        for (int qd = 0; qd < Geo::GPT; ++qd)
+        for (int qd = 0; qd < Geo::GPT; ++qd) {
+            uint64_t* p = sm + Geo::elem(qd * SC::TB + tib, 0) * 16 + c;
 #pragma unroll
-            for (int k = 0; k < Geo::R; ++k) sm[Geo::elem(qd * SC::TB + tib, k) * 16 + c] = x[qd * Geo::R + k];
+            for (int k = 0; k < Geo::R; ++k) p[k * Geo::s * 16] = x[qd * Geo::R + k];
+        }
     };
 
     if constexpr (!INV) {
@@ -121,6 +136,138 @@ __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>
     }
 }
 
+// ---------------------------------------------------------------- Kernel-1, pipelined
+// Persistent Kernel-1 / Kernel-1': each CTA walks the (row, 16-column tile)
+// pairs prime-major in a grid-stride loop and prefetches the next tile --
+// N1 x 128-byte row segments and the Psi[0..N1) prefix of its prime -- into
+// the other half of a double buffer with cp.async while it transforms the
+// current one.  Round 0 then reads SMEM; the last round stores straight to
+// global (whole 128-byte segments).
+template <int LOGN1, int LOGE>
+struct ColsPipeCfg {
+    using SC = Sched<LOGN1, LOGE>;
+    static constexpr int CT = SC::TB * 16;
+    static constexpr size_t BUF = (size_t)SC::M * 16 * 8 + (size_t)SC::M * sizeof(Tw);  // tile + twiddles
+    static constexpr size_t SMEM = 2 * BUF;
+    static constexpr int MINB = CT <= 256 ? 3 : 1;
+};
+
+template <int LOGN1, int LOGN, int LOGE, bool INV>
+__global__ void __launch_bounds__(ColsPipeCfg<LOGN1, LOGE>::CT, ColsPipeCfg<LOGN1, LOGE>::MINB)
+    k_cols_pipe(const KArgs a)
+{
+    using SC = Sched<LOGN1, LOGE>;
+    using CC = ColsPipeCfg<LOGN1, LOGE>;
+    constexpr int M = SC::M, NR = SC::NR, CT = CC::CT;
+    constexpr uint32_t logn2 = LOGN - LOGN1;
+    extern __shared__ __align__(16) uint64_t sm[];
+    auto tile_of = [&](uint32_t buf) { return sm + buf * (CC::BUF / 8); };
+    auto tw_of = [&](uint32_t buf) { return reinterpret_cast<Tw*>(sm + buf * (CC::BUF / 8) + M * 16); };
+
+    const uint32_t tid = threadIdx.x, c = tid & 15u, tib = tid >> 4;
+    const uint32_t tiles_per_row = 1u << a.log_tiles;
+    const uint32_t total = a.batch * a.L * tiles_per_row;
+
+    auto locate = [&](uint32_t t, uint32_t& l, uint64_t*& base) {
+        const uint32_t tile = t & (tiles_per_row - 1u), q = t >> a.log_tiles;  // q = l * batch + b
+        l = q / a.batch;
+        const uint32_t b = q - l * a.batch;
+        base = a.data + (((uint64_t)b * a.L + l) << LOGN) + tile * 16u;
+    };
+    auto prefetch = [&](uint32_t t, uint32_t buf) {
+        if (t < total) {
+            uint32_t l;
+            uint64_t* base;
+            locate(t, l, base);
+            uint64_t* st = tile_of(buf);
+            // M rows x 8 chunks of 16 bytes; thread tid takes chunks tid, tid+CT, ...
+#pragma unroll
+            for (int j = 0; j < (M * 8) / CT; ++j) {
+                const uint32_t ch = j * CT + tid, row = ch >> 3, col2 = (ch & 7u) * 2;
+                cp_async16(st + row * 16 + col2, base + ((uint64_t)row << logn2) + col2);
+            }
+            const Tw* tab = a.tab + ((uint64_t)l << LOGN);
+            Tw* tw = tw_of(buf);
+            for (uint32_t i = tid; i < (uint32_t)M; i += CT) cp_async16(tw + i, tab + i);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    uint32_t t = blockIdx.x;
+    prefetch(t, 0);
+    for (uint32_t it = 0; t < total; ++it, t += gridDim.x) {
+        const uint32_t buf = it & 1u;
+        prefetch(t + gridDim.x, buf ^ 1u);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();
+
+        uint32_t l;
+        uint64_t* base;
+        locate(t, l, base);
+        uint64_t* col = base + c;
+        uint64_t* smt = tile_of(buf);
+        const Tw* tws = tw_of(buf);
+        const PrimeConst pc = a.pc[l];
+        auto tabf = [&](const TwKey& k) { return tws[k.idx]; };
+        auto otf = [&](uint32_t) { return TwMul<true>{}; };
+
+        uint64_t x[16];
+        auto g_store = [&](auto ri) {
+            using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
+#pragma unroll
+            for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+                for (int k = 0; k < Geo::R; ++k)
+                    col[(uint64_t)Geo::elem(qd * SC::TB + tib, k) << logn2] = x[qd * Geo::R + k];
+        };
+        auto s_load = [&](auto ri) {
+            using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
+#pragma unroll
+            for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+                for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = smt[Geo::elem(qd * SC::TB + tib, k) * 16 + c];
+        };
+        auto s_store = [&](auto ri) {
+            using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
+#pragma unroll
+            for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+                for (int k = 0; k < Geo::R; ++k) smt[Geo::elem(qd * SC::TB + tib, k) * 16 + c] = x[qd * Geo::R + k];
+        };
+
+        if constexpr (!INV) {
+            static_for<NR>([&](auto ri) {
+                constexpr int RI = decltype(ri)::value;
+                s_load(ri);
+                ct_round<LOGN1, LOGE, RI, 1 << 20>(x, tib, 0u, tabf, otf, pc);
+                if constexpr (RI == NR - 1) {
+                    g_store(ri);
+                } else {
+                    s_store(ri);
+                    __syncthreads();
+                }
+            });
+        } else {
+            static_for<NR>([&](auto rj) {
+                constexpr int RI = NR - 1 - decltype(rj)::value;
+                using RC = std::integral_constant<int, RI>;
+                s_load(RC{});
+                gs_round<LOGN1, LOGE, RI, 1 << 20, true>(x, tib, 0u, tabf, otf, pc);
+                if constexpr (RI == 0) {
+#pragma unroll
+                    for (int k = 0; k < SC::E; ++k) x[k] = norm4(x[k], pc);
+                    g_store(RC{});
+                } else {
+                    s_store(RC{});
+                    __syncthreads();
+                }
+            });
+        }
+        __syncthreads();  // this buffer is refilled by the prefetch two iterations on
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- contiguous
 template <int LOGM, int LOGE, bool TWS = false>
 struct ContigCfg {
@@ -132,13 +279,7 @@ struct ContigCfg {
     static constexpr int MINB = CT > 256 ? 1 : (LOGE >= 4 ? 4 : 3);  // register budget
 };
 
-// 16-byte asynchronous global -> shared copy (LDGSTS), and its completion.
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
-{
-    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 
 // Barrier over the TB threads of one block: blocks never share SMEM, so a
 // block that fits one warp synchronises with __syncwarp and larger blocks with
@@ -602,6 +743,34 @@ cudaError_t contig_switch(int logm, const KArgs& a, int ots, uint32_t iters, cud
     return err;
 }
 
+template <int LOGN1, int LOGN, int LOGE, bool INV>
+cudaError_t launch_cols_pipe_t(const KArgs& a, uint32_t rows, cudaStream_t st)
+{
+    using CC = ColsPipeCfg<LOGN1, LOGE>;
+    auto fn = k_cols_pipe<LOGN1, LOGN, LOGE, INV>;
+    static std::atomic<uint64_t> attr_set{0};  // one bit per device
+    static int ctas_per_sm = 0;
+    if (!set_once(attr_set)) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, fn, CC::CT, CC::SMEM);
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t want = (uint64_t)rows << a.log_tiles;
+    const uint64_t grid = std::min<uint64_t>(want, (uint64_t)sms * std::max(1, ctas_per_sm));
+    fn<<<(unsigned)grid, CC::CT, CC::SMEM, st>>>(a);
+    return cudaPeekAtLastError();
+}
+
+template <bool INV, int... Ks>
+cudaError_t cols_pipe_switch(int key, const KArgs& a, uint32_t rows, cudaStream_t st, std::integer_sequence<int, Ks...>)
+{
+    cudaError_t err = cudaErrorInvalidValue;
+    ((key == Ks ? (err = launch_cols_pipe_t<(Ks & 15), (Ks >> 4), 4, INV>(a, rows, st), 0) : 0), ...);
+    return err;
+}
+
 // Ks encodes (logn << 4) | log_n1
 template <int LOGE, bool INV, int... Ks>
 cudaError_t cols_switch(int key, const KArgs& a, uint32_t rows, cudaStream_t st, std::integer_sequence<int, Ks...>)
@@ -646,8 +815,10 @@ cudaError_t launch_k2(bool inverse, int loge, const KArgs& a, int ots, uint32_t 
 
 cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st)
 {
-    (void)loge;  // Kernel-1 runs per-thread radix 16 (the measured best, profiles/)
     const int key = (int)((a.logn << 4) | a.log_n1);
+    if (loge == 5 && a.log_n1 <= 9)  // pipelined persistent Kernel-1 (radix 16); SMEM caps N1 at 2^9
+        return inverse ? cols_pipe_switch<true>(key, a, rows, st, K1Pairs{})
+                       : cols_pipe_switch<false>(key, a, rows, st, K1Pairs{});
     return inverse ? cols_switch<4, true>(key, a, rows, st, K1Pairs{})
                    : cols_switch<4, false>(key, a, rows, st, K1Pairs{});
 }
