@@ -496,10 +496,14 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
 template <int LOGM, int LOGE>
 struct PipeCfg {
     static constexpr int TB = Sched<LOGM, LOGE>::TB;
-    static constexpr int NB = TB >= 64 ? 4 : 4;  // slots per CTA
+    static constexpr int SLOT = (1 << LOGM) * (2 * 8 + 16);  // bytes per slot
+    static constexpr int NB0 = (96 * 1024) / SLOT;
+    static constexpr int NB = NB0 < 1 ? 1 : (NB0 > 4 ? 4 : NB0);  // slots per CTA
     static constexpr int CT = NB * TB;
-    static constexpr size_t SMEM = (size_t)2 * NB * (1 << LOGM) * (8 + sizeof(Tw));
-    static constexpr int MINB = LOGE >= 4 ? 2 : 3;
+    // double-buffered data, single-buffered twiddles (refilled once the last
+    // round has read them): (2 x 8 + 16) x N2 bytes per slot
+    static constexpr size_t SMEM = (size_t)NB * (1 << LOGM) * (2 * 8 + sizeof(Tw));
+    static constexpr int MINB = LOGE >= 4 ? 3 : 3;
 };
 
 template <int LOGM, int LOGE, bool INV, int OTS>
@@ -524,8 +528,8 @@ __global__ void __launch_bounds__(PipeCfg<LOGM, LOGE>::CT, PipeCfg<LOGM, LOGE>::
         const uint32_t b = q - l * a.batch;
         return a.data + (((uint64_t)b * a.L + l) << a.logn) + (uint64_t)bb * M;
     };
-    Tw* const tw_base = reinterpret_cast<Tw*>(sm + 2 * NB * M);
-    auto prefetch = [&](uint32_t gb, uint32_t buf) {
+    Tw* const tws = reinterpret_cast<Tw*>(sm + 2 * NB * M) + blk * M;
+    auto prefetch_data = [&](uint32_t gb, uint32_t buf) {
         if (gb < a.total_blocks) {
             uint32_t l, bb;
             const uint64_t* g = block_ptr(gb, l, bb);
@@ -535,27 +539,31 @@ __global__ void __launch_bounds__(PipeCfg<LOGM, LOGE>::CT, PipeCfg<LOGM, LOGE>::
                 const uint32_t ch = j * TB + tib;
                 cp_async16(sd + swz(2 * ch), g + 2 * ch);
             }
-            const Tw* t2 = a.tab2 + ((uint64_t)l << a.logn) + ((uint64_t)bb << LOGM);
-            Tw* st = tw_base + (buf * NB + blk) * M;
-#pragma unroll
-            for (int j = 0; j < E; ++j) cp_async16(st + j * TB + tib, t2 + j * TB + tib);
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
     };
+    auto prefetch_tw = [&](uint32_t gb) {
+        if (gb < a.total_blocks) {
+            const uint32_t bb = gb & n1mask, q = gb >> a.log_n1, l = q / a.batch;
+            const Tw* t2 = a.tab2 + ((uint64_t)l << a.logn) + ((uint64_t)bb << LOGM);
+#pragma unroll
+            for (int j = 0; j < E; ++j) cp_async16(tws + j * TB + tib, t2 + j * TB + tib);
+        }
+    };
+    auto commit = [] { asm volatile("cp.async.commit_group;" ::: "memory"); };
 
     uint32_t gb = blockIdx.x * NB + blk;
-    prefetch(gb, 0);
+    prefetch_data(gb, 0);
+    prefetch_tw(gb);
+    commit();
     for (uint32_t it = 0; gb < a.total_blocks; ++it, gb += nslots) {
         uint64_t* sb = sm + ((it & 1) * NB + blk) * M;
-        const Tw* tws = tw_base + ((it & 1) * NB + blk) * M;
-        prefetch(gb + nslots, (it + 1) & 1);
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        prefetch_data(gb + nslots, (it + 1) & 1);
+        commit();
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // data(it) and tw(it) landed
         block_sync<TB>(blk);
-
         uint32_t l, bb;
         uint64_t* g = block_ptr(gb, l, bb);
         const uint32_t Fm1 = (1u << a.log_n1) + bb - 1u;
-        const Tw* tab = a.tab + ((uint64_t)l << a.logn);
         const Tw* ot = a.ot + (uint64_t)l * (B_ot + ((1u << a.logn) >> a.ot_logb));
         const PrimeConst pc = a.pc[l];
         // Kernel-2 table segment (plan-built, per block, per round, [i][h][g]),
@@ -623,6 +631,8 @@ __global__ void __launch_bounds__(PipeCfg<LOGM, LOGE>::CT, PipeCfg<LOGM, LOGE>::
                 s_store(ri);
                 block_sync<TB>(blk);
             });
+            prefetch_tw(gb + nslots);  // the sync above ended every twiddle read
+            commit();
             stage_out();
         } else {
             static_for<NR>([&](auto rj) {
@@ -644,6 +654,10 @@ __global__ void __launch_bounds__(PipeCfg<LOGM, LOGE>::CT, PipeCfg<LOGM, LOGE>::
             if constexpr (!DIRECT0) stage_out();
         }
         block_sync<TB>(blk);  // all reads of this buffer done before it is refilled
+        if constexpr (INV) {
+            prefetch_tw(gb + nslots);
+            commit();
+        }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
 }
