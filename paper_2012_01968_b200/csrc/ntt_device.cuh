@@ -231,9 +231,12 @@ struct TwKey {
     uint32_t g;    // group
 };
 
-template <int LOGM, int LOGE, int RI, int OT_FROM, class TabF, class OtF>
-__device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
-                                         const OtF& otf, const PrimeConst& c)
+// NI sub-transforms per thread share every twiddle (Kernel-1 columns of one
+// tile; Kernel-2 blocks of one prime at the same block position): one twiddle
+// load serves NI times the butterflies, and NI independent chains add ILP.
+template <int LOGM, int LOGE, int RI, int OT_FROM, int NI, class TabF, class OtF>
+__device__ __forceinline__ void ct_roundN(uint64_t (&x)[NI][16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
+                                          const OtF& otf, const PrimeConst& c)
 {
     using Geo = RoundGeo<LOGM, RI, LOGE>;
     constexpr int R = Geo::R, S = Geo::S;
@@ -251,24 +254,33 @@ __device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32
                     const TwMul<true> w = otf(idx + (Fm1 << (S + i)));
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
-                        ct_bf(x[qd * R + k], x[qd * R + k + half], w, c);
+#pragma unroll
+                        for (int n = 0; n < NI; ++n) ct_bf(x[n][qd * R + k], x[n][qd * R + k + half], w, c);
                 } else {
                     const TwMul<false> w{tabf(TwKey{idx, S + i, S, i, h, G / Geo::s})};
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
-                        ct_bf(x[qd * R + k], x[qd * R + k + half], w, c);
+#pragma unroll
+                        for (int n = 0; n < NI; ++n) ct_bf(x[n][qd * R + k], x[n][qd * R + k + half], w, c);
                 }
             }
         }
     }
 }
 
+template <int LOGM, int LOGE, int RI, int OT_FROM, class TabF, class OtF>
+__device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
+                                         const OtF& otf, const PrimeConst& c)
+{
+    ct_roundN<LOGM, LOGE, RI, OT_FROM, 1>(reinterpret_cast<uint64_t(&)[1][16]>(x), tib, Fm1, tabf, otf, c);
+}
+
 // Inverse round: the same groups and twiddle indices, Gentleman-Sande stages
 // in reverse order.  FUSE0: local stage 0 is global stage 0 (m = 1), where
 // N^-1 is fused: X' = (X+Y) N^-1, Y' = (X-Y) Psi^-1[1] N^-1 (R15).
-template <int LOGM, int LOGE, int RI, int OT_FROM, bool FUSE0, class TabF, class OtF>
-__device__ __forceinline__ void gs_round(uint64_t (&x)[16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
-                                         const OtF& otf, const PrimeConst& c)
+template <int LOGM, int LOGE, int RI, int OT_FROM, bool FUSE0, int NI, class TabF, class OtF>
+__device__ __forceinline__ void gs_roundN(uint64_t (&x)[NI][16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
+                                          const OtF& otf, const PrimeConst& c)
 {
     using Geo = RoundGeo<LOGM, RI, LOGE>;
     constexpr int R = Geo::R, S = Geo::S;
@@ -282,11 +294,13 @@ __device__ __forceinline__ void gs_round(uint64_t (&x)[16], uint32_t tib, uint32
             if (FUSE0 && S + i == 0) {
                 const TwMul<false> a{c.ninv}, b{c.ninv_psi};
 #pragma unroll
-                for (int k = 0; k < half; ++k) {
-                    const uint64_t u = x[qd * R + k], v = x[qd * R + k + half];
-                    x[qd * R + k] = a.mul(u + v, c);
-                    x[qd * R + k + half] = b.mul(u - v + c.p5, c);
-                }
+                for (int k = 0; k < half; ++k)
+#pragma unroll
+                    for (int n = 0; n < NI; ++n) {
+                        const uint64_t u = x[n][qd * R + k], v = x[n][qd * R + k + half];
+                        x[n][qd * R + k] = a.mul(u + v, c);
+                        x[n][qd * R + k + half] = b.mul(u - v + c.p5, c);
+                    }
                 continue;
             }
 #pragma unroll
@@ -296,16 +310,26 @@ __device__ __forceinline__ void gs_round(uint64_t (&x)[16], uint32_t tib, uint32
                     const TwMul<true> w = otf(idx + (Fm1 << (S + i)));
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
-                        gs_bf(x[qd * R + k], x[qd * R + k + half], w, c);
+#pragma unroll
+                        for (int n = 0; n < NI; ++n) gs_bf(x[n][qd * R + k], x[n][qd * R + k + half], w, c);
                 } else {
                     const TwMul<false> w{tabf(TwKey{idx, S + i, S, i, h, G / Geo::s})};
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
-                        gs_bf(x[qd * R + k], x[qd * R + k + half], w, c);
+#pragma unroll
+                        for (int n = 0; n < NI; ++n) gs_bf(x[n][qd * R + k], x[n][qd * R + k + half], w, c);
                 }
             }
         }
     }
+}
+
+// Inverse round, one sub-transform per thread.
+template <int LOGM, int LOGE, int RI, int OT_FROM, bool FUSE0, class TabF, class OtF>
+__device__ __forceinline__ void gs_round(uint64_t (&x)[16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
+                                         const OtF& otf, const PrimeConst& c)
+{
+    gs_roundN<LOGM, LOGE, RI, OT_FROM, FUSE0, 1>(reinterpret_cast<uint64_t(&)[1][16]>(x), tib, Fm1, tabf, otf, c);
 }
 
 // Canonical reduction at the end of a direction, for any x < 2^64:
