@@ -124,6 +124,21 @@ ntt_status_t ntt_inverse(ntt_plan_t plan, uint64_t *data, unsigned batch, void *
 ntt_status_t ntt_launch_pass(ntt_plan_t plan, uint64_t *data, unsigned batch, unsigned dir, unsigned pass,
                              void *stream);
 
+/* ntt_forward_variant -- the forward transform through one of the paper's
+ * comparison implementations, rebuilt for sm_100a, for
+ * the paper's radix-2 vs SMEM ratio (Table 2):
+ *   NTT_VARIANT_DEFAULT  (0): the two-kernel SMEM path (== ntt_forward);
+ *   NTT_VARIANT_RADIX2   (1): Algorithm 1, one launch per stage, every
+ *                             butterfly through global memory;
+ *   NTT_VARIANT_RADIX16  (2): register-based radix-16 passes, no shared
+ *                             memory, ceil(log2 N / 4) launches.
+ * Output identical to ntt_forward (bit-exact).  Same data contract and errors,
+ * plus INVALID_ARG for an unknown variant. */
+#define NTT_VARIANT_DEFAULT 0u
+#define NTT_VARIANT_RADIX2 1u
+#define NTT_VARIANT_RADIX16 2u
+ntt_status_t ntt_forward_variant(ntt_plan_t plan, uint64_t *data, unsigned batch, unsigned variant, void *stream);
+
 /* ntt_execute_host -- the end-to-end path with HOST buffers: for each chunk of
  * ciphertexts, copy host_in -> device workspace, run the requested transforms
  * (flags: NTT_DIR_FORWARD, NTT_DIR_INVERSE, or both = forward then inverse),

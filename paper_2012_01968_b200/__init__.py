@@ -121,6 +121,14 @@ class Plan:
               "ntt_launch_pass")
         return x
 
+    def forward_variant(self, x, variant: int, stream=None):
+        """Forward NTT through one of the paper's comparison kernels
+        (1 = radix-2 per stage, 2 = register radix-16; 0 = default path)."""
+        ptr, batch = _dev_ptr(x, self.N, self.L)
+        check(lib().ntt_forward_variant(self.handle, ptr, batch, variant, _stream_handle(stream)),
+              "ntt_forward_variant")
+        return x
+
     def workspace_words(self, batch: int, chunk: int = 0) -> int:
         return int(lib().ntt_workspace_words(self.handle, batch, chunk))
 

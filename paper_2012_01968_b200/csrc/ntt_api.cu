@@ -415,6 +415,18 @@ ntt_status_t ntt_launch_pass(ntt_plan_t plan, uint64_t* data, unsigned batch, un
     return run(plan, data, batch, stream, dir == NTT_DIR_INVERSE, plan->log_n1 == 0 ? -1 : (int)pass);
 }
 
+ntt_status_t ntt_forward_variant(ntt_plan_t plan, uint64_t* data, unsigned batch, unsigned variant, void* stream)
+{
+    if (variant == NTT_VARIANT_DEFAULT) return ntt_forward(plan, data, batch, stream);
+    if (!plan || !data || variant > NTT_VARIANT_RADIX16) return NTT_ERR_INVALID_ARG;
+    if (batch == 0) return NTT_OK;
+    ntt_status_t s = check_data(plan, data);
+    if (s != NTT_OK) return s;
+    DeviceGuard g(plan->device);
+    const KArgs a = base_args(plan, data, batch, false);
+    return ntt::launch_baseline_forward((int)variant, a, (cudaStream_t)stream) == cudaSuccess ? NTT_OK : NTT_ERR_CUDA;
+}
+
 static unsigned auto_chunk(const ntt_plan_s* plan, unsigned batch, unsigned chunk)
 {
     if (chunk) return std::min(chunk, batch);

@@ -218,6 +218,22 @@ def test_full_size_configs(name, ot):
     assert np.array_equal(to_host(d), x)
 
 
+@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("logn", [1, 3, 4, 6, 10, 13, 14, 17])
+def test_paper_baseline_kernels(variant, logn):
+    """The paper's radix-2 (Algorithm 1 per stage) and register radix-16
+    comparison kernels (NEXT-3) are bit-exact with the oracle."""
+    N = 1 << logn
+    primes, psis = chain(N, 3)
+    x = synth.rns_rows(primes, 2, N, config_id=11)
+    plan = Plan(N, primes)
+    d = to_dev(x)
+    plan.forward_variant(d, variant)
+    assert np.array_equal(to_host(d), oracle.ntt_batch(x.copy(), primes, psis, +1))
+    plan.inverse(d)
+    assert np.array_equal(to_host(d), x)
+
+
 @pytest.mark.parametrize("L", [1, 2, 7, 16, 45])
 def test_c5_prime_sweep(L):
     """BASELINE.json C5 (mixed stream): N=2^16, one ciphertext per request,
