@@ -124,6 +124,25 @@ ntt_status_t ntt_inverse(ntt_plan_t plan, uint64_t *data, unsigned batch, void *
 ntt_status_t ntt_launch_pass(ntt_plan_t plan, uint64_t *data, unsigned batch, unsigned dir, unsigned pass,
                              void *stream);
 
+/* ntt_pointwise_inverse -- data <- iNTT(a_ntt (.) data): the element-wise
+ * product in the NTT domain followed by the inverse, i.e. the
+ * output side of a negacyclic polynomial product.  The
+ * product (Montgomery, R = 2^64; the R^-1 is folded into the inverse's N^-1)
+ * is fused into the inverse's first kernel when the plan runs without OT,
+ * otherwise it is a separate element-wise kernel.
+ *   a_ntt, data: DEVICE pointers, layout as ntt_forward, both in the
+ *   bit-reversed NTT domain with words in [0, p) (as ntt_forward returns);
+ *   a_ntt is read only; data is overwritten with canonical coefficients.
+ * Errors: as ntt_forward. */
+ntt_status_t ntt_pointwise_inverse(ntt_plan_t plan, const uint64_t *a_ntt, uint64_t *data, unsigned batch,
+                                   void *stream);
+
+/* ntt_negacyclic_mul -- b <- a * b mod (X^N + 1, p_l) for every row:
+ * ntt_forward(a), ntt_forward(b), ntt_pointwise_inverse(a, b).  On return a
+ * holds NTT(a) (bit-reversed) and b the product's coefficients in [0, p).
+ * a and b must be distinct.  Errors: as ntt_forward, INVALID_ARG if a == b. */
+ntt_status_t ntt_negacyclic_mul(ntt_plan_t plan, uint64_t *a, uint64_t *b, unsigned batch, void *stream);
+
 /* ntt_forward_variant -- the forward transform through one of the paper's
  * comparison implementations, rebuilt for sm_100a, for
  * the paper's radix-2 vs SMEM ratio (Table 2):

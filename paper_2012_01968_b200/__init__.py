@@ -121,6 +121,25 @@ class Plan:
               "ntt_launch_pass")
         return x
 
+    def pointwise_inverse(self, a_ntt, x, stream=None):
+        """x <- iNTT(a_ntt (.) x): both CUDA tensors in the NTT domain."""
+        pa, batch_a = _dev_ptr(a_ntt, self.N, self.L)
+        ptr, batch = _dev_ptr(x, self.N, self.L)
+        if batch_a != batch:
+            raise ValueError("operands must have the same batch")
+        check(lib().ntt_pointwise_inverse(self.handle, pa, ptr, batch, _stream_handle(stream)),
+              "ntt_pointwise_inverse")
+        return x
+
+    def negacyclic_mul(self, a, b, stream=None):
+        """b <- a * b mod (X^N + 1) per row; a is left in the NTT domain."""
+        pa, batch_a = _dev_ptr(a, self.N, self.L)
+        pb, batch = _dev_ptr(b, self.N, self.L)
+        if batch_a != batch:
+            raise ValueError("operands must have the same batch")
+        check(lib().ntt_negacyclic_mul(self.handle, pa, pb, batch, _stream_handle(stream)), "ntt_negacyclic_mul")
+        return b
+
     def forward_variant(self, x, variant: int, stream=None):
         """Forward NTT through one of the paper's comparison kernels
         (1 = radix-2 per stage, 2 = register radix-16; 0 = default path)."""

@@ -22,7 +22,8 @@ NTT_VARIANT_DEFAULT, NTT_VARIANT_RADIX2, NTT_VARIANT_RADIX16 = 0, 1, 2
 # every symbol include/ntt.h declares
 EXPORTS = [
     "ntt_find_primes", "ntt_find_psi", "ntt_plan_create", "ntt_plan_create_ex", "ntt_plan_psi",
-    "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_launch_pass", "ntt_forward_variant", "ntt_execute_host", "ntt_workspace_words",
+    "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_launch_pass", "ntt_pointwise_inverse", "ntt_negacyclic_mul", "ntt_forward_variant",
+    "ntt_execute_host", "ntt_workspace_words",
     "ntt_plan_destroy", "ntt_status_string",
 ]
 
@@ -64,6 +65,8 @@ def lib() -> ctypes.CDLL:
         L.ntt_inverse.argtypes = [vp, vp, u32, vp]
         L.ntt_launch_pass.argtypes = [vp, vp, u32, u32, u32, vp]
         L.ntt_forward_variant.argtypes = [vp, vp, u32, u32, vp]
+        L.ntt_pointwise_inverse.argtypes = [vp, vp, vp, u32, vp]
+        L.ntt_negacyclic_mul.argtypes = [vp, vp, vp, u32, vp]
         L.ntt_execute_host.argtypes = [vp, u32, vp, vp, u32, vp, u64, u32]
         L.ntt_workspace_words.argtypes = [vp, u32, u32]
         L.ntt_workspace_words.restype = u64
@@ -71,7 +74,8 @@ def lib() -> ctypes.CDLL:
         L.ntt_status_string.argtypes = [i32]
         L.ntt_status_string.restype = ctypes.c_char_p
         for name in ["ntt_find_primes", "ntt_find_psi", "ntt_plan_create", "ntt_plan_create_ex",
-                     "ntt_plan_psi", "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_launch_pass", "ntt_forward_variant", "ntt_execute_host",
+                     "ntt_plan_psi", "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_launch_pass", "ntt_forward_variant",
+                     "ntt_pointwise_inverse", "ntt_negacyclic_mul", "ntt_execute_host",
                      "ntt_plan_destroy"]:
             getattr(L, name).restype = i32
         _lib = L

@@ -30,7 +30,8 @@ struct ntt_plan_s {
     Tw* d_inv2 = nullptr;
     Tw* d_ot_fwd = nullptr;  // [L][B + N/B]
     Tw* d_ot_inv = nullptr;
-    PrimeConst* d_pc = nullptr;  // [L]
+    PrimeConst* d_pc = nullptr;       // [L]
+    PrimeConst* d_pc_mont = nullptr;  // [L] the same with N^-1 scaled by 2^64 (NTT-domain products)
     uint64_t table_bytes = 0;
     int loge_k1 = 4, loge_k2 = 5;  // Kernel-1 radix exponent; Kernel-2 variant (5 = pipelined radix-16)
 };
@@ -107,6 +108,8 @@ void free_plan_memory(ntt_plan_s* p)
     cudaFree(p->d_ot_fwd);
     cudaFree(p->d_ot_inv);
     cudaFree(p->d_pc);
+    cudaFree(p->d_pc_mont);
+    p->d_pc_mont = nullptr;
     cudaFree(p->d_fwd2);
     cudaFree(p->d_inv2);
     p->d_fwd2 = p->d_inv2 = nullptr;
@@ -145,16 +148,29 @@ KArgs base_args(const ntt_plan_s* plan, uint64_t* data, unsigned batch, bool inv
     return a;
 }
 
-// Enqueue one direction (pass < 0: all passes) on `st`; no checks.
+// Enqueue one direction (pass < 0: all passes) on `st`; no checks.  mul_a:
+// fuse data <- mul_a (.) data into the inverse's first kernel (Montgomery,
+// with the R-scaled N^-1 constants).
 cudaError_t enqueue(const ntt_plan_s* plan, uint64_t* data, unsigned batch, bool inverse, cudaStream_t st,
-                    int pass = -1)
+                    int pass = -1, const uint64_t* mul_a = nullptr)
 {
     KArgs a = base_args(plan, data, batch, inverse);
+    if (mul_a) {
+        a.pc = plan->d_pc_mont;
+        a.mul_a = mul_a;
+    }
     const uint32_t rows = batch * plan->L;
     const int ots = plan->ot_enable ? (int)plan->ot_stages : 0;
     if (plan->log_n1 == 0) {
         a.total_blocks = rows;
-        return ntt::launch_single(inverse, a, ots, 1, st);
+        cudaError_t e = ntt::launch_single(inverse, a, ots, 1, st);
+        if (e == cudaErrorNotSupported && mul_a) {  // unfused: product kernel, then the inverse
+            cudaGetLastError();
+            if ((e = ntt::launch_pointwise(a, st)) != cudaSuccess) return e;
+            a.mul_a = nullptr;
+            e = ntt::launch_single(inverse, a, ots, 1, st);
+        }
+        return e;
     }
     a.total_blocks = rows << plan->log_n1;
     a.log_tiles = plan->logn - plan->log_n1 - 4;
@@ -164,7 +180,18 @@ cudaError_t enqueue(const ntt_plan_s* plan, uint64_t* data, unsigned batch, bool
         if (pass != 0) e = ntt::launch_k2(false, plan->loge_k2, a, ots, 1, st);
         return e;
     }
-    if (pass != 1 && (e = ntt::launch_k2(true, plan->loge_k2, a, ots, 1, st)) != cudaSuccess) return e;
+    if (pass != 1) {
+        e = ntt::launch_k2(true, plan->loge_k2, a, ots, 1, st);
+        if (e == cudaErrorNotSupported && mul_a) {  // unfused: product kernel, then Kernel-2'
+            cudaGetLastError();
+            if ((e = ntt::launch_pointwise(a, st)) != cudaSuccess) return e;
+            KArgs b = a;
+            b.mul_a = nullptr;
+            e = ntt::launch_k2(true, plan->loge_k2, b, ots, 1, st);
+        }
+        if (e != cudaSuccess) return e;
+    }
+    a.mul_a = nullptr;
     if (pass != 0) e = ntt::launch_k1(true, plan->loge_k1, a, rows, st);
     return e;
 }
@@ -298,7 +325,7 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
     // host tables, one thread per hardware thread over primes
     const uint64_t N = n, NOT = ot_base + N / ot_base;
     std::vector<Tw> h_fwd(N * L), h_inv(N * L), h_otf(NOT * L), h_oti(NOT * L);
-    std::vector<PrimeConst> h_pc(L);
+    std::vector<PrimeConst> h_pc(L), h_pcm(L);
     unsigned nth = std::max(1u, std::min(L, std::thread::hardware_concurrency()));
     std::vector<std::thread> th;
     for (unsigned t = 0; t < nth; ++t)
@@ -323,10 +350,22 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
                 c.p5 = 5 * q;
                 c.p4_hi = (uint32_t)((4 * q) >> 32);
                 c.rn = (uint32_t)((((unsigned __int128)1) << 90) / q);
+                uint64_t inv = 1;  // p^-1 mod 2^64 by Newton iteration (p odd)
+                for (int it = 0; it < 6; ++it) inv *= 2 - q * inv;
+                c.pinv = 0 - inv;
+                c.pad2 = 0;
                 nttp::Twiddle t1 = nttp::shoup_pair(ninv, q), t2 = nttp::shoup_pair(ninv_psi, q);
                 c.ninv = Tw{t1.w, t1.wb};
                 c.ninv_psi = Tw{t2.w, t2.wb};
                 h_pc[l] = c;
+                // R-scaled copy for inverses fed by Montgomery products (R = 2^64)
+                const uint64_t r_mod = (uint64_t)((((unsigned __int128)1) << 64) % q);
+                PrimeConst cm = c;
+                nttp::Twiddle t3 = nttp::shoup_pair(nttp::mul_mod(ninv, r_mod, q), q);
+                nttp::Twiddle t4 = nttp::shoup_pair(nttp::mul_mod(ninv_psi, r_mod, q), q);
+                cm.ninv = Tw{t3.w, t3.wb};
+                cm.ninv_psi = Tw{t4.w, t4.wb};
+                h_pcm[l] = cm;
             }
         });
     for (auto& t : th) t.join();
@@ -352,7 +391,7 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
     const size_t bt = sizeof(Tw) * N * L, bo = sizeof(Tw) * NOT * L, bp = sizeof(PrimeConst) * L;
     if (cudaMalloc(&p->d_fwd, bt) != cudaSuccess || cudaMalloc(&p->d_inv, bt) != cudaSuccess ||
         cudaMalloc(&p->d_ot_fwd, bo) != cudaSuccess || cudaMalloc(&p->d_ot_inv, bo) != cudaSuccess ||
-        cudaMalloc(&p->d_pc, bp) != cudaSuccess ||
+        cudaMalloc(&p->d_pc, bp) != cudaSuccess || cudaMalloc(&p->d_pc_mont, bp) != cudaSuccess ||
         (k2tab && (cudaMalloc(&p->d_fwd2, bt) != cudaSuccess || cudaMalloc(&p->d_inv2, bt) != cudaSuccess))) {
         cudaGetLastError();
         free_plan_memory(p);
@@ -364,6 +403,7 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
         cudaMemcpy(p->d_ot_fwd, h_otf.data(), bo, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(p->d_ot_inv, h_oti.data(), bo, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(p->d_pc, h_pc.data(), bp, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(p->d_pc_mont, h_pcm.data(), bp, cudaMemcpyHostToDevice) != cudaSuccess ||
         (k2tab && (cudaMemcpy(p->d_fwd2, h_fwd2.data(), bt, cudaMemcpyHostToDevice) != cudaSuccess ||
                    cudaMemcpy(p->d_inv2, h_inv2.data(), bt, cudaMemcpyHostToDevice) != cudaSuccess))) {
         cudaGetLastError();
@@ -413,6 +453,28 @@ ntt_status_t ntt_launch_pass(ntt_plan_t plan, uint64_t* data, unsigned batch, un
     if (!plan || (dir != NTT_DIR_FORWARD && dir != NTT_DIR_INVERSE)) return NTT_ERR_INVALID_ARG;
     if (pass > 1 || (pass == 1 && plan->log_n1 == 0)) return NTT_ERR_INVALID_ARG;
     return run(plan, data, batch, stream, dir == NTT_DIR_INVERSE, plan->log_n1 == 0 ? -1 : (int)pass);
+}
+
+ntt_status_t ntt_pointwise_inverse(ntt_plan_t plan, const uint64_t* a_ntt, uint64_t* data, unsigned batch,
+                                   void* stream)
+{
+    if (!plan || !data || !a_ntt) return NTT_ERR_INVALID_ARG;
+    if (batch == 0) return NTT_OK;
+    ntt_status_t s = check_data(plan, data);
+    if (s == NTT_OK) s = check_data(plan, a_ntt);
+    if (s != NTT_OK) return s;
+    DeviceGuard g(plan->device);
+    return enqueue(plan, data, batch, true, (cudaStream_t)stream, -1, a_ntt) == cudaSuccess ? NTT_OK : NTT_ERR_CUDA;
+}
+
+ntt_status_t ntt_negacyclic_mul(ntt_plan_t plan, uint64_t* a, uint64_t* b, unsigned batch, void* stream)
+{
+    if (!plan || !a || !b) return NTT_ERR_INVALID_ARG;
+    if (a == b) return NTT_ERR_INVALID_ARG;
+    ntt_status_t s;
+    if ((s = ntt_forward(plan, a, batch, stream)) != NTT_OK) return s;
+    if ((s = ntt_forward(plan, b, batch, stream)) != NTT_OK) return s;
+    return ntt_pointwise_inverse(plan, a, b, batch, stream);
 }
 
 ntt_status_t ntt_forward_variant(ntt_plan_t plan, uint64_t* data, unsigned batch, unsigned variant, void* stream)

@@ -23,8 +23,10 @@ struct __align__(16) PrimeConst {
     uint64_t p5;         // 5p: the GS difference offset (section 5.1)
     uint32_t p4_hi;      // high word of 4p
     uint32_t rn;         // floor(2^90 / p): quotient estimate for the final reduction
-    Tw ninv;             // N^-1
+    Tw ninv;             // N^-1   [R-scaled copy: N^-1 2^64, see mont_mul]
     Tw ninv_psi;         // N^-1 * Psi^-1[1], the fused last GS stage (R15)
+    uint64_t pinv;       // -p^-1 mod 2^64 (Montgomery, NTT-domain products)
+    uint64_t pad2;
 };
 
 // Kernel arguments (passed by value, lives in the constant bank).
@@ -40,6 +42,7 @@ struct KArgs {
     uint32_t iters;         // contig kernel: block-groups per CTA
     uint32_t ot_logb;       // OT: log2 of the base B
     uint32_t total_blocks;  // contig kernel: rows * N1
+    const uint64_t* mul_a;  // fused NTT-domain product: the other operand, same layout as data
 };
 
 // ------------------------------------------------------------ arithmetic
@@ -86,6 +89,18 @@ __device__ __forceinline__ uint64_t shoup_lazy(uint64_t b, uint64_t w, uint64_t 
 }
 
 __device__ __forceinline__ uint64_t csub(uint64_t x, uint64_t m) { return x >= m ? x - m : x; }
+
+// Element-wise product of two NTT-domain operands (the odot) --
+// both vary, so Shoup does not apply; Montgomery with R = 2^64:
+//   T = a b,  m = T mod 2^64 * (-p^-1),  (T + m p) / 2^64 = a b 2^-64 mod p,
+// in [0, 2p) for a, b < p.  The 2^-64 is undone by an R-scaled N^-1 in the
+// inverse that follows (ntt_pointwise_inverse).
+__device__ __forceinline__ uint64_t mont_mul(uint64_t a, uint64_t b, const PrimeConst& c)
+{
+    const uint64_t lo = a * b, hi = __umul64hi(a, b);
+    const uint64_t m = lo * c.pinv;
+    return hi + __umul64hi(m, c.p) + (lo != 0);
+}
 
 // Conditional subtraction decided on the high words only: subtracts m iff
 // hi(x) > hi(m) (then x > m).  The result is < max(x - m, m + 2^32): an

@@ -299,7 +299,7 @@ __device__ __forceinline__ void block_sync(uint32_t blk)
 // contiguous table ranges, copied with cp.async into a local table
 // tl[2^j + h] at the block's start (one latency per block instead of one per
 // round) and read back with LDS.128.  Stages under OT skip their ranges.
-template <int LOGM, int LOGE, bool INV, bool FUSE0, int OTS, bool TWS>
+template <int LOGM, int LOGE, bool INV, bool FUSE0, int OTS, bool TWS, bool MUL = false>
 __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM, LOGE, TWS>::MINB)
     k_contig(const KArgs a)
 {
@@ -361,7 +361,12 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
 #pragma unroll
             for (int j = 0; j < E / 2; ++j) {
                 const uint32_t ch = j * TB + tib;
-                const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(g + 2 * ch);
+                ulonglong2 v = *reinterpret_cast<const ulonglong2*>(g + 2 * ch);
+                if constexpr (MUL) {  // fused NTT-domain product (ntt_pointwise_inverse)
+                    const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(a.mul_a + (g - a.data) + 2 * ch);
+                    v.x = mont_mul(u.x, v.x, pc);
+                    v.y = mont_mul(u.y, v.y, pc);
+                }
                 *reinterpret_cast<ulonglong2*>(sb + swz(2 * ch)) = v;
             }
             block_sync<TB>(blk);
@@ -506,7 +511,7 @@ struct PipeCfg {
     static constexpr int MINB = LOGE >= 4 ? 3 : 3;
 };
 
-template <int LOGM, int LOGE, bool INV, int OTS>
+template <int LOGM, int LOGE, bool INV, int OTS, bool MUL = false>
 __global__ void __launch_bounds__(PipeCfg<LOGM, LOGE>::CT, PipeCfg<LOGM, LOGE>::MINB) k_blocks(const KArgs a)
 {
     using SC = Sched<LOGM, LOGE>;
@@ -639,6 +644,15 @@ __global__ void __launch_bounds__(PipeCfg<LOGM, LOGE>::CT, PipeCfg<LOGM, LOGE>::
                 constexpr int RI = NR - 1 - decltype(rj)::value;
                 using RC = std::integral_constant<int, RI>;
                 s_load(RC{});
+                if constexpr (MUL && RI == NR - 1) {  // fused NTT-domain product (ntt_pointwise_inverse)
+                    using Geo = RoundGeo<LOGM, RI, LOGE>;
+                    const uint64_t* ga = a.mul_a + (g - a.data);
+#pragma unroll
+                    for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+                        for (int k = 0; k < Geo::R; ++k)
+                            x[qd * Geo::R + k] = mont_mul(__ldg(ga + Geo::elem(qd * TB + tib, k)), x[qd * Geo::R + k], pc);
+                }
                 gs_round<LOGM, LOGE, RI, OT_FROM, false>(x, tib, Fm1, tabf, otf, pc);
                 if constexpr (RI == 0 && DIRECT0) {
                     using Geo = RoundGeo<LOGM, 0, LOGE>;
@@ -660,6 +674,30 @@ __global__ void __launch_bounds__(PipeCfg<LOGM, LOGE>::CT, PipeCfg<LOGM, LOGE>::
         }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- element-wise product
+// b <- a (.) b 2^-64 for every word (unfused path of ntt_pointwise_inverse;
+// rows [batch][L][N], row (b, l) mod primes[l]).
+__global__ void __launch_bounds__(256) k_pointwise(const KArgs a, uint64_t words)
+{
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (2 * i >= words) return;
+    const uint32_t l = (uint32_t)((2 * i >> a.logn) % a.L);
+    const PrimeConst pc = a.pc[l];
+    const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(a.mul_a + 2 * i);
+    ulonglong2 v = *reinterpret_cast<const ulonglong2*>(a.data + 2 * i);
+    v.x = mont_mul(u.x, v.x, pc);
+    v.y = mont_mul(u.y, v.y, pc);
+    *reinterpret_cast<ulonglong2*>(a.data + 2 * i) = v;
+}
+
+cudaError_t launch_pointwise(const KArgs& a, cudaStream_t st)
+{
+    const uint64_t words = ((uint64_t)a.batch * a.L) << a.logn;
+    const uint64_t threads = (words + 1) / 2;
+    k_pointwise<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(a, words);
+    return cudaPeekAtLastError();
 }
 
 // ---------------------------------------------------------------- dispatch
@@ -686,11 +724,11 @@ cudaError_t launch_cols_t(const KArgs& a, uint32_t rows, cudaStream_t st)
     return cudaPeekAtLastError();
 }
 
-template <int LOGM, int LOGE, bool INV, bool FUSE0, int OTS, bool TWS>
+template <int LOGM, int LOGE, bool INV, bool FUSE0, int OTS, bool TWS, bool MUL = false>
 cudaError_t launch_contig_t(KArgs a, uint32_t iters, cudaStream_t st)
 {
     using CC = ContigCfg<LOGM, LOGE, TWS>;
-    auto fn = k_contig<LOGM, LOGE, INV, FUSE0, OTS, TWS>;
+    auto fn = k_contig<LOGM, LOGE, INV, FUSE0, OTS, TWS, MUL>;
     static std::atomic<uint64_t> attr_set{0};  // one bit per device
     if (!set_once(attr_set)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
     a.iters = iters;
@@ -700,11 +738,11 @@ cudaError_t launch_contig_t(KArgs a, uint32_t iters, cudaStream_t st)
     return cudaPeekAtLastError();
 }
 
-template <int LOGM, int LOGE, bool INV, int OTS>
+template <int LOGM, int LOGE, bool INV, int OTS, bool MUL = false>
 cudaError_t launch_blocks_t(KArgs a, cudaStream_t st)
 {
     using PC = PipeCfg<LOGM, LOGE>;
-    auto fn = k_blocks<LOGM, LOGE, INV, OTS>;
+    auto fn = k_blocks<LOGM, LOGE, INV, OTS, MUL>;
     static std::atomic<uint64_t> attr_set{0};  // one bit per device
     static int ctas_per_sm = 0;
     if (!set_once(attr_set)) {
@@ -723,6 +761,12 @@ cudaError_t launch_blocks_t(KArgs a, cudaStream_t st)
 template <int LOGM, int LOGE, bool INV>
 cudaError_t launch_blocks_ot(const KArgs& a, int ots, cudaStream_t st)
 {
+    if (a.mul_a) {  // fused product only in the radix-16 inverse without OT; else the caller unfuses
+        if constexpr (INV && LOGE == 4) {
+            if (ots == 0) return launch_blocks_t<LOGM, LOGE, INV, 0, true>(a, st);
+        }
+        return cudaErrorNotSupported;
+    }
     switch (ots) {
         case 0: return launch_blocks_t<LOGM, LOGE, INV, 0>(a, st);
         case 1: return launch_blocks_t<LOGM, LOGE, INV, 1>(a, st);
@@ -741,6 +785,12 @@ cudaError_t blocks_switch(int logm, const KArgs& a, int ots, cudaStream_t st, st
 template <int LOGM, int LOGE, bool INV, bool FUSE0, bool TWS>
 cudaError_t launch_contig_ot(const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
 {
+    if (a.mul_a) {  // fused product only in the radix-16 inverse without OT; else the caller unfuses
+        if constexpr (INV && LOGE == 4) {
+            if (ots == 0) return launch_contig_t<LOGM, LOGE, INV, FUSE0, 0, TWS, true>(a, iters, st);
+        }
+        return cudaErrorNotSupported;
+    }
     switch (ots) {
         case 0: return launch_contig_t<LOGM, LOGE, INV, FUSE0, 0, TWS>(a, iters, st);
         case 1: return launch_contig_t<LOGM, LOGE, INV, FUSE0, 1, TWS>(a, iters, st);

@@ -12,6 +12,8 @@ cudaError_t launch_single(bool inverse, const KArgs& a, int ot_stages, uint32_t 
 cudaError_t launch_k2(bool inverse, int loge, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
 // Kernel-1 (forward) / Kernel-1' (inverse): stride-N2 columns, 16 per CTA.
 cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st);
+// data <- mul_a (.) data 2^-64 (Montgomery), every word.
+cudaError_t launch_pointwise(const KArgs& a, cudaStream_t st);
 // The paper's comparison kernels, forward only: 1 = radix-2 per stage, 2 = register radix-16.
 cudaError_t launch_baseline_forward(int variant, const KArgs& a, cudaStream_t st);
 }  // namespace ntt

@@ -218,6 +218,52 @@ def test_full_size_configs(name, ot):
     assert np.array_equal(to_host(d), x)
 
 
+@pytest.mark.parametrize("logn,kw", [(1, {}), (4, {}), (8, {}), (10, {}), (10, {"ot": True}), (13, {}),
+                                     (14, {}), (14, {"ot": True}), (16, {}), (17, {"log_n1": 9})])
+def test_negacyclic_mul(logn, kw):
+    """NEXT-2: b <- a*b mod (X^N+1) with the product fused into the inverse:
+    equals the oracle's schoolbook product for small N and, for large
+    N, the oracle pipeline NTT -> odot -> iNTT (whose convolution-theorem
+    equality the oracle tests pin)."""
+    N = 1 << logn
+    primes, psis = chain(N, 2)
+    a = synth.rns_rows(primes, 2, N, config_id=12)
+    b = synth.rns_rows(primes, 2, N, config_id=13)
+    plan = Plan(N, primes, **kw)
+    da, db = to_dev(a), to_dev(b)
+    plan.negacyclic_mul(da, db)
+    got = to_host(db)
+    A = oracle.ntt_batch(a.copy(), primes, psis, +1)
+    assert np.array_equal(to_host(da), A)  # a left in the NTT domain
+    if logn <= 10:
+        for bi in range(2):
+            for l in range(2):
+                assert np.array_equal(got[bi, l], oracle.negacyclic_mul(a[bi, l], b[bi, l], primes[l]))
+    else:
+        B = oracle.ntt_batch(b.copy(), primes, psis, +1)
+        C = np.stack([np.stack([oracle.pointwise_mul(A[bi, l], B[bi, l], primes[l]) for l in range(2)])
+                      for bi in range(2)])
+        assert np.array_equal(got, oracle.ntt_batch(C, primes, psis, -1))
+
+
+@pytest.mark.parametrize("variant", ["4,3", "4,6", "4,4"])
+def test_negacyclic_mul_unfused_variants(variant, monkeypatch):
+    """Kernel-2 variants without the fused product fall back to a separate
+    element-wise kernel: same result."""
+    monkeypatch.setenv("NTT_LOGE", variant)
+    N = 1 << 15
+    primes, psis = chain(N, 2)
+    a = synth.rns_rows(primes, 1, N, config_id=12)
+    b = synth.rns_rows(primes, 1, N, config_id=13)
+    plan = Plan(N, primes)
+    da, db = to_dev(a), to_dev(b)
+    plan.negacyclic_mul(da, db)
+    A = oracle.ntt_batch(a.copy(), primes, psis, +1)
+    B = oracle.ntt_batch(b.copy(), primes, psis, +1)
+    C = np.stack([oracle.pointwise_mul(A[0, l], B[0, l], primes[l]) for l in range(2)])[None]
+    assert np.array_equal(to_host(db), oracle.ntt_batch(C, primes, psis, -1))
+
+
 @pytest.mark.parametrize("variant", [1, 2])
 @pytest.mark.parametrize("logn", [1, 3, 4, 6, 10, 13, 14, 17])
 def test_paper_baseline_kernels(variant, logn):

@@ -209,6 +209,24 @@ __global__ void k_bfw(uint64_t* out, uint64_t p, uint64_t w, uint64_t wb) {
   for (int c = 0; c < CH; ++c) s ^= X[c] ^ Y[c];
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
+// the paper's "native modulo" comparison: same butterfly with the
+// product reduced by the compiler's 128-by-64-bit remainder instead of Shoup
+__global__ void k_bf_native(uint64_t* out, uint64_t p, uint64_t w, uint64_t wb) {
+  uint64_t X[CH], Y[CH];
+  for (int c = 0; c < CH; ++c) { X[c] = (threadIdx.x * 77 + c) % p; Y[c] = (threadIdx.x * 31 + c * 5) % p; }
+  for (int it = 0; it < ITERS / 8; ++it)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const uint64_t t = (uint64_t)(((unsigned __int128)Y[c] * w) % p);
+      const uint64_t x = X[c];
+      X[c] = x + t >= p ? x + t - p : x + t;
+      Y[c] = x >= t ? x - t : x + p - t;
+    }
+  uint64_t s = 0;
+  for (int c = 0; c < CH; ++c) s ^= X[c] ^ Y[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 // correctness of the FP64 quotient variant against exact arithmetic (host check)
 __global__ void k_f64check(uint64_t* bad, const uint64_t* bs, uint64_t p, uint64_t w, uint64_t wb, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -345,6 +363,17 @@ int main() {
     uint64_t nb = 0;
     cudaMemcpy(&nb, bad, 8, cudaMemcpyDeviceToHost);
     printf("{\"check\": \"shoup_f64\", \"n\": %d, \"bad\": %llu}\n", n, (unsigned long long)nb);
+  }
+  {
+    for (int rep = 0; rep < 2; ++rep) k_bf_native<<<blocks, threads>>>(out, p, w, wb);
+    cudaEventRecord(e0);
+    k_bf_native<<<blocks, threads>>>(out, p, w, wb);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double ops = (double)blocks * threads * (ITERS / 8) * CH;
+    printf("{\"kernel\": \"ct_native_mod\", \"Gops_per_s\": %.1f}\n", ops / ms / 1e6);
   }
   // occupancy sweep for the PTX butterfly: warps per SM vs rate
   for (int wps : {4, 8, 12, 16, 24, 32, 48, 64}) {
