@@ -197,9 +197,17 @@ def run_own(args):
     if world != args.gpus:
         if world == 1 and args.gpus > 1:
             raise SystemExit("--gpus N>1 needs torchrun --nproc-per-node N")
+    # BENCH_DIST_BACKEND=gloo (testing only): several ranks sharing the visible
+    # GPUs, reductions on CPU tensors; the default is one rank per GPU over NCCL.
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    red_dev = "cuda" if backend == "nccl" else "cpu"
 
     logn, L_total, batch_per_gpu, text = CONFIGS[args.config]
     N = 1 << logn
@@ -245,7 +253,7 @@ def run_own(args):
         per_kernel = [statistics.mean(ev[s][j].elapsed_time(ev[s][j + 1]) for s in range(steps))
                       for j in range(len(seq))]
         if world > 1:
-            t = torch.tensor([ms], device="cuda")
+            t = torch.tensor([ms], device=red_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         names = [("fwd" if d == NTT_DIR_FORWARD else "inv") + f"_pass{p}" for d, p in seq]
@@ -292,6 +300,22 @@ def run_own(args):
     ot_plan.close()
     ot_steps = max(3, args.steps // 2)
 
+    # NEXT-2 context: negacyclic product of two full-L ciphertext batches (fwd a, fwd b, fused odot+inv)
+    pm_steps = max(2, min(args.steps, 5))
+    other = dev.clone()
+    for _ in range(2):
+        plan.negacyclic_mul(other, dev)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(pm_steps):
+        plan.negacyclic_mul(other, dev)
+    e1.record()
+    torch.cuda.synchronize()
+    pm_ms = e0.elapsed_time(e1) / pm_steps
+    del other
+    dev.copy_(host.cuda())
+
     # e2e: host buffers through the public C-ABI host path, H2D + fwd + inv + D2H per step
     out_host = torch.empty_like(host).pin_memory()
     ws = torch.empty(plan.workspace_words(B), dtype=torch.int64, device="cuda")
@@ -304,7 +328,7 @@ def run_own(args):
         plan.execute_host(host, out_host, NTT_DIR_FORWARD | NTT_DIR_INVERSE, ws)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     if world > 1:
-        t = torch.tensor([e2e_s], device="cuda")
+        t = torch.tensor([e2e_s], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_ok = bool(torch.equal(out_host, host))
@@ -351,6 +375,8 @@ def run_own(args):
             "ot_on": {"value": round(ms_ot / ot_steps * 1e3 / units, 3), "unit": "us",
                       "ms_per_step": round(ms_ot / ot_steps, 4),
                       "kernels_ms": {k: round(v, 4) for k, v in kern_ot.items()}},
+            "negacyclic_mul": {"ms_per_step": round(pm_ms, 4), "us_per_ct": round(pm_ms * 1e3 / units, 3),
+                               "what": "b <- a*b mod (X^N+1): 2 forward NTTs + fused odot/inverse, per ciphertext pair"},
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_s * 1e6 / units, 3), "unit": "us",
                     "h2d_bytes_per_step": words * 8, "d2h_bytes_per_step": words * 8,

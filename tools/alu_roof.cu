@@ -160,6 +160,21 @@ __device__ __forceinline__ uint64_t shoup_v4(uint64_t b, uint64_t w, uint64_t wb
       "mov.b64 %0, {r0, r1};\n\t}" : "=l"(r) : "l"(b), "l"(w), "l"(wb), "l"(np));
   return r;
 }
+// V9: r = (b w) + q (-p) with the b w partial products issued before q is known
+// (shorter dependency chain: only 1 WIDE + 2 IMAD after the quotient)
+__device__ __forceinline__ uint64_t shoup_v9(uint64_t b, uint64_t w, uint64_t wb, uint64_t np) {
+  uint64_t r;
+  asm("{\n\t.reg .u32 b0, b1, v0, v1, w0, w1, n0, n1, t0, t1, q0, q1, r0, r1, s1;\n\t.reg .u64 q, a;\n\t"
+      "mov.b64 {b0, b1}, %1;\n\tmov.b64 {w0, w1}, %2;\n\tmov.b64 {v0, v1}, %3;\n\tmov.b64 {n0, n1}, %4;\n\t"
+      "mul.wide.u32 a, b0, w0;\n\tmov.b64 {r0, r1}, a;\n\t"
+      "mad.lo.u32 r1, b0, w1, r1;\n\tmad.lo.u32 r1, b1, w0, r1;\n\tmov.b64 a, {r0, r1};\n\t"
+      "mul.hi.u32 t0, b1, v0;\n\tmul.hi.u32 t1, b0, v1;\n\tmul.wide.u32 q, b1, v1;\n\tmov.b64 {q0, q1}, q;\n\t"
+      "add.cc.u32 q0, q0, t0;\n\taddc.u32 q1, q1, 0;\n\tadd.cc.u32 q0, q0, t1;\n\taddc.u32 q1, q1, 0;\n\t"
+      "mul.lo.u32 s1, q0, n1;\n\tmad.lo.u32 s1, q1, n0, s1;\n\t"
+      "mad.wide.u32 a, q0, n0, a;\n\tmov.b64 {r0, r1}, a;\n\tadd.u32 r1, r1, s1;\n\t"
+      "mov.b64 %0, {r0, r1};\n\t}" : "=l"(r) : "l"(b), "l"(w), "l"(wb), "l"(np));
+  return r;
+}
 __device__ __forceinline__ uint64_t shoup_f64(uint64_t b, uint64_t w, uint64_t wb, uint64_t np, double V0, double V1) {
   const uint32_t b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
   const double two52 = 4503599627370496.0;
@@ -202,7 +217,7 @@ __global__ void k_bfw(uint64_t* out, uint64_t p, uint64_t w, uint64_t wb) {
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
       uint64_t x = csub_hi(X[c], p5, p5h);
-      uint64_t t = V == 4 ? shoup_v4(Y[c], w, wb, np) : V == 5 ? shoup_f64(Y[c], w, wb, np, V0, V1) : shoup_f64b(Y[c], w, wb, np, V0, V1);
+      uint64_t t = V == 4 ? shoup_v4(Y[c], w, wb, np) : V == 9 ? shoup_v9(Y[c], w, wb, np) : V == 5 ? shoup_f64(Y[c], w, wb, np, V0, V1) : shoup_f64b(Y[c], w, wb, np, V0, V1);
       X[c] = x + t; Y[c] = x - t + p5;
     }
   uint64_t s = 0;
@@ -375,6 +390,23 @@ int main() {
     double ops = (double)blocks * threads * (ITERS / 8) * CH;
     printf("{\"kernel\": \"ct_native_mod\", \"Gops_per_s\": %.1f}\n", ops / ms / 1e6);
   }
+  // occupancy sweep: kernel-path butterfly (V4) vs shorter-chain variant (V9)
+  for (int v : {4, 9})
+    for (int wps : {8, 12, 16, 32, 64}) {
+      int thr = 128, bps = wps * 32 / thr;
+      int nb = sms * bps;
+      for (int rep = 0; rep < 2; ++rep) {
+        if (v == 4) k_bfw<4><<<nb, thr>>>(out, p, w, wb); else k_bfw<9><<<nb, thr>>>(out, p, w, wb);
+      }
+      cudaEventRecord(e0);
+      if (v == 4) k_bfw<4><<<nb, thr>>>(out, p, w, wb); else k_bfw<9><<<nb, thr>>>(out, p, w, wb);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      double ops = (double)nb * thr * ITERS * CH;
+      printf("{\"kernel\": \"ct_w%d_occ\", \"warps_per_sm\": %d, \"Gops_per_s\": %.1f}\n", v, wps, ops / ms / 1e6);
+    }
   // occupancy sweep for the PTX butterfly: warps per SM vs rate
   for (int wps : {4, 8, 12, 16, 24, 32, 48, 64}) {
     int thr = 128, bps = wps * 32 / thr;
