@@ -75,13 +75,15 @@ void build_k2_table(const Tw* std_tab, unsigned logn, unsigned log_n1, unsigned 
         Tw* o = out + (uint64_t)bb * N2;
         o[0] = Tw{0, 0};
         uint32_t off = 1;
-        for (unsigned S = 0; S < logm; S += le) {
-            const unsigned r = std::min(le, logm - S);
+        const unsigned rem = logm % le;  // remainder round first (ntt::Sched)
+        for (unsigned S = 0; S < logm;) {
+            const unsigned r = (S == 0 && rem) ? rem : le;
             for (unsigned i = 0; i < r; ++i)
                 for (uint32_t h = 0; h < (1u << i); ++h)
                     for (uint32_t g = 0; g < (1u << S); ++g)
                         o[off + ((((1u << i) - 1u + h) << S) + g)] = std_tab[((((uint64_t)F << S) + g) << i) + h];
             off += ((1u << r) - 1u) << S;
+            S += r;
         }
     }
 }

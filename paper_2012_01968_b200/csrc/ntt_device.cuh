@@ -185,10 +185,14 @@ struct Sched {
     static constexpr int M = 1 << LOGM;
     static constexpr int LE = LOGM < LOGE ? LOGM : LOGE;
     static constexpr int E = 1 << LE;
-    static constexpr int NR = (LOGM + LE - 1) / LE;
+    // A remainder round (LOGM mod LE stages) goes FIRST in forward order: its
+    // stages have the fewest distinct twiddles (one per block for the first
+    // stage), so the many-twiddle last stages run inside full radix-E rounds.
+    static constexpr int REM = LOGM % LE;
+    static constexpr int NR = LOGM / LE + (REM ? 1 : 0);
     static constexpr int TB = M / E;  // threads per sub-transform
-    static constexpr int r(int i) { return (LOGM - LE * i) < LE ? (LOGM - LE * i) : LE; }
-    static constexpr int S(int i) { return LE * i; }
+    __host__ __device__ static constexpr int r(int i) { return (REM && i == 0) ? REM : LE; }
+    __host__ __device__ static constexpr int S(int i) { return (REM && i > 0) ? REM + LE * (i - 1) : LE * i; }
 };
 
 // Geometry of round RI (stages [S, S+r) of the sub-transform, S = LE RI): the
@@ -219,14 +223,11 @@ struct RoundGeo {
 // Entry 0 is padding.  Host and device share this definition.
 template <int LOGM, int LOGE>
 struct K2Layout {
-    static constexpr int LE = LOGM < LOGE ? LOGM : LOGE;
+    using SC = Sched<LOGM, LOGE>;
     __host__ __device__ static constexpr uint32_t round_off(int S)
     {
         uint32_t off = 1;
-        for (int s0 = 0; s0 < S; s0 += LE) {
-            const int r = (LOGM - s0) < LE ? (LOGM - s0) : LE;
-            off += ((1u << r) - 1u) << s0;
-        }
+        for (int i = 0; i < SC::NR && SC::S(i) < S; ++i) off += ((1u << SC::r(i)) - 1u) << SC::S(i);
         return off;
     }
 };
