@@ -274,9 +274,9 @@ struct ContigCfg {
     static constexpr int TB = Sched<LOGM, LOGE>::TB;
     static constexpr int CT = TB > 256 ? TB : 256;  // threads per CTA
     static constexpr int NB = CT / TB;              // blocks per CTA iteration
-    // data words, plus (TWS) each block's local twiddle table of M entries
-    static constexpr size_t SMEM = (size_t)NB * (1 << LOGM) * (8 + (TWS ? sizeof(Tw) : 0));
-    static constexpr int MINB = CT > 256 ? 1 : (LOGE >= 4 ? 4 : 3);  // register budget
+    static constexpr size_t SMEM = (size_t)NB * (1 << LOGM) * 8;  // data words
+    // register budget: the Kernel-2 mode (TWS) targets 32 warps/SM like Kernel-1
+    static constexpr int MINB = CT > 256 ? 1 : (TWS ? 4 : (LOGE >= 4 ? 2 : 3));
 };
 
 
@@ -311,7 +311,6 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
 
     const uint32_t tid = threadIdx.x, blk = tid / TB, tib = tid % TB;
     uint64_t* sb = sm + blk * M;
-    Tw* tl = reinterpret_cast<Tw*>(sm + CC::NB * M) + blk * M;
     const uint32_t n1mask = (1u << a.log_n1) - 1u;
     const uint32_t B_ot = 1u << a.ot_logb;
 
@@ -326,21 +325,12 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
         const Tw* tab = a.tab + ((uint64_t)l << a.logn);
         const Tw* ot = a.ot + (uint64_t)l * (B_ot + ((1u << a.logn) >> a.ot_logb));
         const PrimeConst pc = a.pc[l];
-        if constexpr (TWS) {
-            // local stages j < OT_FROM: tl[2^j + h] <- Psi[F 2^j + h]
-            constexpr int NT = (OT_FROM < LOGM ? (1 << OT_FROM) : M) - 1;  // entries 1..NT
-#pragma unroll
-            for (int u = 0; u < (NT + TB - 1) / TB; ++u) {
-                const uint32_t t = 1 + u * TB + tib;
-                if (t <= (uint32_t)NT) {
-                    const uint32_t j = 31 - __clz(t), h = t - (1u << j);
-                    cp_async16(tl + t, tab + ((F << j) + h));
-                }
-            }
-        }
+        // TWS (Kernel-2 mode): twiddles from the plan's Kernel-2 table, whose
+        // per-round [i][h][g] order makes every warp read contiguous entries.
+        const Tw* tb2 = a.tab2 + ((uint64_t)l << a.logn) + ((uint64_t)bb << LOGM);
         auto tabf = [&](const TwKey& k) {
             if constexpr (TWS) {
-                return tl[k.idx];
+                return ldg_tw(tb2 + K2Layout<LOGM, LOGE>::round_off(k.S) + ((((1u << k.i) - 1u + k.h) << k.S) + k.g));
             } else {
                 return ldg_tw(tab + k.idx + ((F - 1u) << k.j));
             }
@@ -435,12 +425,7 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
             }
         };
 
-        auto tw_ready = [&]() {
-            if constexpr (TWS) {
-                cp_async_wait_all();
-                block_sync<TB>(blk);
-            }
-        };
+        auto tw_ready = [&]() {};
         if constexpr (!INV) {
             if constexpr (!DIRECT0) stage_in();
             tw_ready();
