@@ -688,6 +688,20 @@ cudaError_t launch_pointwise(const KArgs& a, cudaStream_t st)
 // ---------------------------------------------------------------- dispatch
 namespace {
 
+// SM count of the current device, cached per device (persistent-grid sizing)
+int sm_count()
+{
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int v = cache[dev & 63].load(std::memory_order_relaxed);
+    if (v == 0) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev & 63].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+
 // true if this device already had the attribute set; marks it otherwise
 bool set_once(std::atomic<uint64_t>& mask)
 {
@@ -734,9 +748,7 @@ cudaError_t launch_blocks_t(KArgs a, cudaStream_t st)
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC::SMEM);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, fn, PC::CT, PC::SMEM);
     }
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = sm_count();
     const uint64_t want = ((uint64_t)a.total_blocks + PC::NB - 1) / PC::NB;
     const uint64_t grid = std::min<uint64_t>(want, (uint64_t)sms * std::max(1, ctas_per_sm));
     fn<<<(unsigned)grid, PC::CT, PC::SMEM, st>>>(a);
@@ -803,9 +815,7 @@ cudaError_t launch_cols_pipe_t(const KArgs& a, uint32_t rows, cudaStream_t st)
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, fn, CC::CT, CC::SMEM);
     }
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = sm_count();
     const uint64_t want = (uint64_t)rows << a.log_tiles;
     const uint64_t grid = std::min<uint64_t>(want, (uint64_t)sms * std::max(1, ctas_per_sm));
     fn<<<(unsigned)grid, CC::CT, CC::SMEM, st>>>(a);
