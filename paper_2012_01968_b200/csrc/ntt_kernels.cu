@@ -276,7 +276,7 @@ struct ContigCfg {
     static constexpr int NB = CT / TB;              // blocks per CTA iteration
     static constexpr size_t SMEM = (size_t)NB * (1 << LOGM) * 8;  // data words
     // register budget: the Kernel-2 mode (TWS) targets 32 warps/SM like Kernel-1
-    static constexpr int MINB = CT > 256 ? 1 : (TWS ? 4 : (LOGE >= 4 ? 2 : 3));
+    static constexpr int MINB = CT > 256 ? 1 : (TWS ? 3 : (LOGE >= 4 ? 2 : 3));
 };
 
 
