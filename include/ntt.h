@@ -180,6 +180,51 @@ uint64_t ntt_workspace_words(ntt_plan_t plan, unsigned batch, unsigned chunk);
  * NULL is accepted (no-op).  Caller must have synchronised all work. */
 ntt_status_t ntt_plan_destroy(ntt_plan_t plan);
 
+/* ---------------------------------------------------------------- 32-bit words
+ * The paper's 32-bit-word alternative ("32b vs 64b"; SURVEY 8(f)
+ * NEXT-4): residues of primes 2^29 <= p < 2^30 stored one per uint32 word, with
+ * 32-bit Shoup pairs w_bar = floor(w 2^32 / p) (Algorithm 4, with
+ * beta = 2^32).  A modulus Q of the same size needs about twice as many primes
+ * as the 60-bit path.  The transform, its order and its canonical output are
+ * those of ntt_forward / ntt_inverse (R4, R5, R10, R15); no
+ * OT and no fused product on this path.  Same general rules as above. */
+typedef struct ntt32_plan_s *ntt32_plan_t;
+
+/* ntt_find_primes32 -- host helper: the first `count` primes p = 1 (mod 2N),
+ * 2^29 <= p < 2^30, scanning downward from 2^30 - 2N + 1, into out[0..count).
+ * Errors: INVALID_N, INVALID_ARG (out == NULL or count == 0), RANGE_EXHAUSTED. */
+ntt_status_t ntt_find_primes32(unsigned n, unsigned count, uint32_t *out);
+
+/* ntt_plan_create32 -- plan for N = n and primes[0..L) (each prime, = 1 mod 2N,
+ * < 2^30, distinct; copied).  Builds, on the current device, Psi / Psi^-1
+ * bit-reversed tables with 32-bit Shoup companions (8 bytes per entry), their
+ * Kernel-2 ordered copies for N >= 2^14, and N^-1.  log_n1: two-kernel split
+ * N = N1 N2; 0 = default (7 for N <= 2^15, else 8), otherwise one
+ * of (N, log_n1) = (2^14, 7), (2^15, 7), (2^16, 8), (2^17, 8), (2^17, 9);
+ * ignored for N <= 2^13 (one kernel holds the row).  Synchronous.
+ * Errors: INVALID_ARG (NULLs, L == 0, unsupported split), INVALID_N,
+ * INVALID_PRIME, CUDA (no device), OOM. */
+ntt_status_t ntt_plan_create32(ntt32_plan_t *plan, unsigned n, const uint32_t *primes, unsigned L,
+                               unsigned log_n1);
+
+/* ntt_plan_info32 -- host query: L, log2 N, log2 N1 used (0 = one kernel),
+ * the plan's psi per prime into psi_out[0..L) (host), device-table bytes.
+ * Any output pointer may be NULL. */
+ntt_status_t ntt_plan_info32(ntt32_plan_t plan, unsigned *L, unsigned *logn, unsigned *log_n1,
+                             uint32_t *psi_out, uint64_t *table_bytes);
+
+/* ntt_forward32 / ntt_inverse32 -- in-place forward / inverse over batch x L
+ * rows of N uint32 words, [b][l][i] row-major, DEVICE pointer on the plan's
+ * device, 16-byte aligned; inputs in [0, p) (precondition), outputs canonical
+ * in [0, p), forward output bit-reversed as ntt_forward.  Asynchronous on
+ * `stream` (cudaStream_t as void*).  batch == 0 is a no-op.
+ * Errors: INVALID_ARG, MISALIGNED, WRONG_DEVICE, CUDA. */
+ntt_status_t ntt_forward32(ntt32_plan_t plan, uint32_t *data, unsigned batch, void *stream);
+ntt_status_t ntt_inverse32(ntt32_plan_t plan, uint32_t *data, unsigned batch, void *stream);
+
+/* ntt_plan_destroy32 -- frees the plan (NULL accepted).  Work must be done. */
+ntt_status_t ntt_plan_destroy32(ntt32_plan_t plan);
+
 /* Static English text for a status code. */
 const char *ntt_status_string(ntt_status_t s);
 

@@ -16,13 +16,21 @@ import ctypes
 
 from ._native import NTT_DIR_FORWARD, NTT_DIR_INVERSE, NttError, Opts, check, lib
 
-__all__ = ["Plan", "find_primes", "find_psi", "NttError", "NTT_DIR_FORWARD", "NTT_DIR_INVERSE"]
+__all__ = ["Plan", "Plan32", "find_primes", "find_primes32", "find_psi", "NttError", "NTT_DIR_FORWARD",
+           "NTT_DIR_INVERSE"]
 
 
 def find_primes(N: int, count: int) -> list[int]:
     """First ``count`` primes p = 1 mod 2N in [2^59, 2^60), descending (host)."""
     out = (ctypes.c_uint64 * count)()
     check(lib().ntt_find_primes(N, count, out), "ntt_find_primes")
+    return [int(v) for v in out]
+
+
+def find_primes32(N: int, count: int) -> list[int]:
+    """First ``count`` primes p = 1 mod 2N in [2^29, 2^30), descending (host)."""
+    out = (ctypes.c_uint32 * count)()
+    check(lib().ntt_find_primes32(N, count, out), "ntt_find_primes32")
     return [int(v) for v in out]
 
 
@@ -33,14 +41,15 @@ def find_psi(p: int, N: int) -> int:
     return int(v.value)
 
 
-def _dev_ptr(t, N: int, L: int) -> tuple[int, int]:
-    """(data_ptr, batch) of a CUDA [batch][L][N] 64-bit tensor."""
+def _dev_ptr(t, N: int, L: int, bits: int = 64) -> tuple[int, int]:
+    """(data_ptr, batch) of a CUDA [batch][L][N] tensor of 64- (or 32-) bit words."""
     import torch
 
     if not isinstance(t, torch.Tensor):
         raise TypeError("expected a torch CUDA tensor")
-    if t.dtype not in (torch.uint64, torch.int64):
-        raise TypeError(f"dtype must be uint64 or int64, got {t.dtype}")
+    ok = (torch.uint64, torch.int64) if bits == 64 else (torch.uint32, torch.int32)
+    if t.dtype not in ok:
+        raise TypeError(f"dtype must be uint{bits} or int{bits}, got {t.dtype}")
     if not t.is_cuda:
         raise ValueError("tensor must be on a CUDA device (no CPU fallback)")
     if not t.is_contiguous():
@@ -170,6 +179,67 @@ class Plan:
     def close(self) -> None:
         if getattr(self, "_h", None) is not None:
             lib().ntt_plan_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Plan32:
+    """The 32-bit-word path (ntt_plan_create32): primes in [2^29, 2^30), one
+    uint32 (or int32) word per residue, ``[batch][L][N]``.  Same transform and
+    output order as :class:`Plan`; no OT, no fused products."""
+
+    def __init__(self, N: int, primes, log_n1: int = 0):
+        self.N = int(N)
+        self.primes = [int(p) for p in primes]
+        self.L = len(self.primes)
+        arr = (ctypes.c_uint32 * max(self.L, 1))(*self.primes)
+        h = ctypes.c_void_p()
+        check(lib().ntt_plan_create32(ctypes.byref(h), self.N, arr, self.L, log_n1), "ntt_plan_create32")
+        self._h = h
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        if self._h is None:
+            raise ValueError("plan destroyed")
+        return self._h
+
+    def info(self) -> dict:
+        L, logn, logn1 = (ctypes.c_uint() for _ in range(3))
+        psi = (ctypes.c_uint32 * self.L)()
+        tb = ctypes.c_uint64()
+        check(lib().ntt_plan_info32(self.handle, ctypes.byref(L), ctypes.byref(logn), ctypes.byref(logn1), psi,
+                                    ctypes.byref(tb)), "ntt_plan_info32")
+        return {"L": L.value, "logn": logn.value, "log_n1": logn1.value, "psis": [int(v) for v in psi],
+                "table_bytes": tb.value}
+
+    @property
+    def psis(self) -> list[int]:
+        return self.info()["psis"]
+
+    def forward(self, x, stream=None):
+        ptr, batch = _dev_ptr(x, self.N, self.L, 32)
+        check(lib().ntt_forward32(self.handle, ptr, batch, _stream_handle(stream)), "ntt_forward32")
+        return x
+
+    def inverse(self, x, stream=None):
+        ptr, batch = _dev_ptr(x, self.N, self.L, 32)
+        check(lib().ntt_inverse32(self.handle, ptr, batch, _stream_handle(stream)), "ntt_inverse32")
+        return x
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None:
+            lib().ntt_plan_destroy32(self._h)
             self._h = None
 
     def __enter__(self):

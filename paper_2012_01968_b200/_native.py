@@ -25,6 +25,8 @@ EXPORTS = [
     "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_launch_pass", "ntt_pointwise_inverse", "ntt_negacyclic_mul", "ntt_forward_variant",
     "ntt_execute_host", "ntt_workspace_words",
     "ntt_plan_destroy", "ntt_status_string",
+    "ntt_find_primes32", "ntt_plan_create32", "ntt_plan_info32", "ntt_forward32", "ntt_inverse32",
+    "ntt_plan_destroy32",
 ]
 
 
@@ -71,12 +73,20 @@ def lib() -> ctypes.CDLL:
         L.ntt_workspace_words.argtypes = [vp, u32, u32]
         L.ntt_workspace_words.restype = u64
         L.ntt_plan_destroy.argtypes = [vp]
+        p32 = ctypes.POINTER(ctypes.c_uint32)
+        L.ntt_find_primes32.argtypes = [u32, u32, p32]
+        L.ntt_plan_create32.argtypes = [pp, u32, p32, u32, u32]
+        L.ntt_plan_info32.argtypes = [vp, ctypes.POINTER(u32), ctypes.POINTER(u32), ctypes.POINTER(u32), p32, p64]
+        L.ntt_forward32.argtypes = [vp, vp, u32, vp]
+        L.ntt_inverse32.argtypes = [vp, vp, u32, vp]
+        L.ntt_plan_destroy32.argtypes = [vp]
         L.ntt_status_string.argtypes = [i32]
         L.ntt_status_string.restype = ctypes.c_char_p
         for name in ["ntt_find_primes", "ntt_find_psi", "ntt_plan_create", "ntt_plan_create_ex",
                      "ntt_plan_psi", "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_launch_pass", "ntt_forward_variant",
                      "ntt_pointwise_inverse", "ntt_negacyclic_mul", "ntt_execute_host",
-                     "ntt_plan_destroy"]:
+                     "ntt_plan_destroy", "ntt_find_primes32", "ntt_plan_create32", "ntt_plan_info32",
+                     "ntt_forward32", "ntt_inverse32", "ntt_plan_destroy32"]:
             getattr(L, name).restype = i32
         _lib = L
     return _lib

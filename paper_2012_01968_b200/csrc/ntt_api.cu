@@ -63,31 +63,6 @@ unsigned default_log_n1(unsigned logn)
     }
 }
 
-// Kernel-2 twiddle order (ntt::K2Layout, runtime form): block bb of a row owns
-// N2 entries; round (S, r) stores Psi[(((F << S) + g) << i) + h] at
-// off(S) + ((2^i - 1 + h) << S) + g, F = N1 + bb.
-void build_k2_table(const Tw* std_tab, unsigned logn, unsigned log_n1, unsigned loge, Tw* out)
-{
-    const unsigned logm = logn - log_n1, le = std::min(loge, logm);
-    const uint32_t N1 = 1u << log_n1, N2 = 1u << logm;
-    for (uint32_t bb = 0; bb < N1; ++bb) {
-        const uint32_t F = N1 + bb;
-        Tw* o = out + (uint64_t)bb * N2;
-        o[0] = Tw{0, 0};
-        uint32_t off = 1;
-        const unsigned rem = logm % le;  // remainder round first (ntt::Sched)
-        for (unsigned S = 0; S < logm;) {
-            const unsigned r = (S == 0 && rem) ? rem : le;
-            for (unsigned i = 0; i < r; ++i)
-                for (uint32_t h = 0; h < (1u << i); ++h)
-                    for (uint32_t g = 0; g < (1u << S); ++g)
-                        o[off + ((((1u << i) - 1u + h) << S) + g)] = std_tab[((((uint64_t)F << S) + g) << i) + h];
-            off += ((1u << r) - 1u) << S;
-            S += r;
-        }
-    }
-}
-
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev)
@@ -218,13 +193,13 @@ const char* ntt_status_string(ntt_status_t s)
     switch (s) {
         case NTT_OK: return "ok";
         case NTT_ERR_INVALID_N: return "N must be a power of two in [2, 2^17]";
-        case NTT_ERR_INVALID_PRIME: return "prime must be prime, = 1 mod 2N, < 2^60 and distinct";
+        case NTT_ERR_INVALID_PRIME: return "prime must be prime, = 1 mod 2N, < 2^60 (32-bit path: < 2^30) and distinct";
         case NTT_ERR_INVALID_ARG: return "invalid argument";
         case NTT_ERR_MISALIGNED: return "data pointer must be 16-byte aligned";
         case NTT_ERR_WRONG_DEVICE: return "data pointer is not device memory of the plan's device";
         case NTT_ERR_CUDA: return "CUDA error";
         case NTT_ERR_OOM: return "out of memory";
-        case NTT_ERR_RANGE_EXHAUSTED: return "not enough NTT primes in [2^59, 2^60)";
+        case NTT_ERR_RANGE_EXHAUSTED: return "not enough NTT primes in the word's range ([2^59, 2^60) or [2^29, 2^30))";
     }
     return "unknown status";
 }
@@ -383,8 +358,8 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
         for (unsigned t = 0; t < nth; ++t)
             th2.emplace_back([&, t] {
                 for (unsigned l = t; l < L; l += nth) {
-                    build_k2_table(&h_fwd[l * N], logn, log_n1, loge, &h_fwd2[l * N]);
-                    build_k2_table(&h_inv[l * N], logn, log_n1, loge, &h_inv2[l * N]);
+                    nttp::k2_order(&h_fwd[l * N], logn, log_n1, loge, &h_fwd2[l * N]);
+                    nttp::k2_order(&h_inv[l * N], logn, log_n1, loge, &h_inv2[l * N]);
                 }
             });
         for (auto& t : th2) t.join();

@@ -45,6 +45,24 @@ struct KArgs {
     const uint64_t* mul_a;  // fused NTT-domain product: the other operand, same layout as data
 };
 
+// 32-bit-word path (ntt32.cu): 30-bit primes, w_bar = floor(w 2^32 / p).
+struct __align__(8) Tw32 {
+    uint32_t w, wb;
+};
+struct __align__(16) PrimeConst32 {
+    uint32_t p, p2;
+    Tw32 ninv;      // N^-1
+    Tw32 ninv_psi;  // N^-1 * Psi^-1[1]
+    uint32_t pad[2];
+};
+struct KArgs32 {
+    uint32_t* data;          // [batch][L][N] 32-bit words
+    const Tw32* tab;         // [L][N] Psi / Psi^-1
+    const Tw32* tab2;        // [L][N1][N2] Kernel-2 order
+    const PrimeConst32* pc;  // [L]
+    uint32_t L, batch, logn, log_n1, log_tiles, total_blocks;
+};
+
 // ------------------------------------------------------------ arithmetic
 // Shoup's modmul (Algorithm 4) with the lazy output of R8 and a
 // truncated quotient: for any b < 2^64 and

@@ -16,4 +16,6 @@ cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cud
 cudaError_t launch_pointwise(const KArgs& a, cudaStream_t st);
 // The paper's comparison kernels, forward only: 1 = radix-2 per stage, 2 = register radix-16.
 cudaError_t launch_baseline_forward(int variant, const KArgs& a, cudaStream_t st);
+// 32-bit-word path: all passes of one direction.
+cudaError_t launch32(bool inverse, const KArgs32& a, uint32_t rows, cudaStream_t st);
 }  // namespace ntt

@@ -61,6 +61,27 @@ bool ntt_primes(uint64_t N, unsigned count, std::vector<uint64_t>& out)
     return true;
 }
 
+bool ntt_primes32(uint64_t N, unsigned count, std::vector<uint32_t>& out)
+{
+    out.clear();
+    const uint64_t lo = 1ull << 29, step = 2 * N;
+    for (uint64_t c = (1ull << 30) - step + 1; out.size() < count; c -= step) {
+        if (c < lo || c > (1ull << 30)) return false;
+        if (is_prime_u64(c)) out.push_back((uint32_t)c);
+    }
+    return true;
+}
+
+bool valid_ntt_prime32(uint64_t p, uint64_t N)
+{
+    return p < (1ull << 30) && p > 2 && (p - 1) % (2 * N) == 0 && is_prime_u64(p);
+}
+
+Twiddle32 shoup_pair32(uint32_t w, uint32_t p)
+{
+    return Twiddle32{w, (uint32_t)(((uint64_t)w << 32) / p)};
+}
+
 bool valid_ntt_prime(uint64_t p, uint64_t N)
 {
     return p < (1ull << 60) && p > 2 && (p - 1) % (2 * N) == 0 && is_prime_u64(p);

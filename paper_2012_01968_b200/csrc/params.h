@@ -22,6 +22,42 @@ Twiddle shoup_pair(uint64_t w, uint64_t p);
 // Returns false if the range is exhausted before `count` primes.
 bool ntt_primes(uint64_t N, unsigned count, std::vector<uint64_t>& out);
 
+// 32-bit word path (NEXT-4): primes p = 1 mod 2N in [2^29, 2^30), descending
+// from 2^30 - 2N + 1; and the 32-bit Shoup pair wb = floor(w 2^32 / p).
+bool ntt_primes32(uint64_t N, unsigned count, std::vector<uint32_t>& out);
+bool valid_ntt_prime32(uint64_t p, uint64_t N);
+struct Twiddle32 {
+    uint32_t w, wb;
+};
+Twiddle32 shoup_pair32(uint32_t w, uint32_t p);
+
+// Kernel-2 twiddle order (ntt::K2Layout, runtime form): block bb of a row owns
+// N2 = 2^(logn - log_n1) entries; round (S, r) of the remainder-first radix-2^loge
+// schedule stores Psi[(((F << S) + g) << i) + h] at off(S) + ((2^i - 1 + h) << S) + g,
+// F = N1 + bb.  T is the table entry type (64- or 32-bit Shoup pair).
+template <class T>
+void k2_order(const T* std_tab, unsigned logn, unsigned log_n1, unsigned loge, T* out)
+{
+    const unsigned logm = logn - log_n1, le = loge < logm ? loge : logm;
+    const uint32_t N1 = 1u << log_n1, N2 = 1u << logm;
+    for (uint32_t bb = 0; bb < N1; ++bb) {
+        const uint32_t F = N1 + bb;
+        T* o = out + (uint64_t)bb * N2;
+        o[0] = T{0, 0};
+        uint32_t off = 1;
+        const unsigned rem = logm % le;
+        for (unsigned S = 0; S < logm;) {
+            const unsigned r = (S == 0 && rem) ? rem : le;
+            for (unsigned i = 0; i < r; ++i)
+                for (uint32_t h = 0; h < (1u << i); ++h)
+                    for (uint32_t g = 0; g < (1u << S); ++g)
+                        o[off + ((((1u << i) - 1u + h) << S) + g)] = std_tab[((((uint64_t)F << S) + g) << i) + h];
+            off += ((1u << r) - 1u) << S;
+            S += r;
+        }
+    }
+}
+
 // Smallest primitive 2N-th root of unity mod p (R2); 0 if none.
 uint64_t smallest_psi(uint64_t p, uint64_t N);
 

@@ -2,6 +2,7 @@
 header declares, and its host-only logic (prime scan, psi, argument checks)
 behaves; no compute call needs a GPU here."""
 import ctypes
+import glob
 import os
 import re
 
@@ -15,9 +16,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def header_functions():
-    src = open(os.path.join(ROOT, "include", "ntt.h")).read()
+    src = "".join(open(f).read() for f in sorted(glob.glob(os.path.join(ROOT, "include", "*.h"))))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(ntt_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(ntt_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_library_loads_and_exports_every_declared_symbol():
@@ -104,6 +105,36 @@ def test_no_cpu_fallback_without_device():
     p = oracle.find_primes(1 << 12, 1)
     arr = (ctypes.c_uint64 * 1)(*p)
     assert lib.ntt_plan_create(ctypes.byref(h), 1 << 12, arr, 1) == -6      # NTT_ERR_CUDA, loudly
+
+
+@pytest.mark.parametrize("logn,count", [(1, 3), (12, 8), (16, 60), (17, 120)])
+def test_host_primes32_match_oracle(logn, count):
+    from paper_2012_01968_b200 import find_primes32
+    N = 1 << logn
+    assert find_primes32(N, count) == oracle.find_primes(N, count, 1 << 29, 1 << 30)
+
+
+def test_plan_create32_argument_errors():
+    lib = _native.lib()
+    h = ctypes.c_void_p()
+    p = oracle.find_primes(1 << 12, 2, 1 << 29, 1 << 30)
+    arr = (ctypes.c_uint32 * 2)(*p)
+    assert lib.ntt_plan_create32(ctypes.byref(h), 3000, arr, 2, 0) == -1
+    assert lib.ntt_plan_create32(ctypes.byref(h), 1 << 12, None, 2, 0) == -3
+    assert lib.ntt_plan_create32(ctypes.byref(h), 1 << 12, arr, 0, 0) == -3
+    bad = (ctypes.c_uint32 * 2)(p[0], p[0])
+    assert lib.ntt_plan_create32(ctypes.byref(h), 1 << 12, bad, 2, 0) == -2      # repeated
+    big = oracle.find_primes(1 << 12, 1, 1 << 30, 1 << 31)                     # >= 2^30: lazy headroom gone
+    bad = (ctypes.c_uint32 * 1)(big[0])
+    assert lib.ntt_plan_create32(ctypes.byref(h), 1 << 12, bad, 1, 0) == -2
+    q = oracle.find_primes(1 << 16, 1, 1 << 29, 1 << 30)
+    arr = (ctypes.c_uint32 * 1)(*q)
+    assert lib.ntt_plan_create32(ctypes.byref(h), 1 << 16, arr, 1, 9) == -3      # split not compiled
+    out = (ctypes.c_uint32 * 1)()
+    assert lib.ntt_find_primes32(1 << 17, 10**6, (ctypes.c_uint32 * 10**6)()) == -8
+    assert lib.ntt_find_primes32(8, 0, out) == -3
+    assert lib.ntt_forward32(None, None, 1, None) == -3
+    assert lib.ntt_plan_destroy32(None) == 0
 
 
 def test_product_package_does_not_touch_oracle():
