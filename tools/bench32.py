@@ -67,7 +67,8 @@ for bits in (64, 32):
                       "batch": B, "fwd_us": round(fw, 1), "inv_us": round(iv, 1),
                       "us_per_ntt_intt": round(fw + iv, 1), "roundtrip_ok": ok,
                       "Gbf_per_s": round(2 * bf / ((fw + iv) * 1e-6) / 1e9, 1),
-                      "hbm_GBps_min_traffic": round(2 * 2 * d.numel() * d.element_size() / ((fw + iv) * 1e-6) / 1e9, 1),
+                      "hbm_GBps_data": round(2 * (2 if plan.info()["log_n1"] else 1) * 2 * d.numel() * d.element_size()
+                                             / ((fw + iv) * 1e-6) / 1e9, 1),
                       "log_n1": plan.info()["log_n1"]}), flush=True)
     plan.close()
     del d, x0
