@@ -73,25 +73,27 @@ struct KArgs32 {
 //   r = b w - q' p = (b w mod p) + k p,  k in {0,1,2,3}  ->  r in [0, 4p).
 // r is formed mod 2^64 as b w + q' (2^64 - p): 3 IMAD.WIDE, 2 IMAD.HI and
 // 4 IMAD on the multiply pipe.  np = 2^64 - p.  The 64-bit partial product
-// b0 w0 + q0 n0 is accumulated in one register pair (no re-pairing moves).
+// b0 w0 + q0 n0 is accumulated in one register pair (no re-pairing moves);
+// q' is one IMAD.WIDE with a zero-extended addend plus one 64-bit add, which
+// ptxas emits as a 3-input IADD3 / IADD3.X pair (a 32-bit add.cc / addc chain
+// became IMAD.X plus moves on the multiply pipe: -6% fmaheavy).
 __device__ __forceinline__ uint64_t shoup_lazy(uint64_t b, uint64_t w, uint64_t wb, uint64_t np)
 {
     uint64_t r;
     asm("{\n\t"
         ".reg .u32 b0, b1, v0, v1, w0, w1, n0, n1, t0, t1, q0, q1, r0, r1;\n\t"
-        ".reg .u64 q, a;\n\t"
+        ".reg .u64 q, a, t;\n\t"
         "mov.b64 {b0, b1}, %1;\n\t"
         "mov.b64 {w0, w1}, %2;\n\t"
         "mov.b64 {v0, v1}, %3;\n\t"
         "mov.b64 {n0, n1}, %4;\n\t"
         "mul.hi.u32 t0, b1, v0;\n\t"
         "mul.hi.u32 t1, b0, v1;\n\t"
-        "mul.wide.u32 q, b1, v1;\n\t"
+        "cvt.u64.u32 t, t0;\n\t"
+        "mad.wide.u32 q, b1, v1, t;\n\t"
+        "cvt.u64.u32 t, t1;\n\t"
+        "add.u64 q, q, t;\n\t"
         "mov.b64 {q0, q1}, q;\n\t"
-        "add.cc.u32 q0, q0, t0;\n\t"
-        "addc.u32 q1, q1, 0;\n\t"
-        "add.cc.u32 q0, q0, t1;\n\t"
-        "addc.u32 q1, q1, 0;\n\t"
         "mul.wide.u32 a, b0, w0;\n\t"
         "mad.wide.u32 a, q0, n0, a;\n\t"
         "mov.b64 {r0, r1}, a;\n\t"
@@ -157,20 +159,30 @@ struct TwMul<true> {
 template <class W>
 __device__ __forceinline__ void ct_bf(uint64_t& X, uint64_t& Y, const W& w, const PrimeConst& c)
 {
-    const uint64_t x = csub_hi(X, c.p4, c.p4_hi);
+    // the conditional subtraction folded into both outputs as 3-input adds
+    // (IADD3 / IADD3.X on the ALU pipe; a 2-input 64-bit add lets ptxas emit
+    // IMAD.X on the multiply pipe, the binding one)
+    const bool ge = (uint32_t)(X >> 32) > c.p4_hi;
+    const uint64_t s = ge ? c.p4 : 0, s2 = ge ? 0 : c.p4;
     const uint64_t t = w.mul(Y, c);
-    X = x + t;
-    Y = x - t + c.p4;
+    const uint64_t x = X;
+    X = x - s + t;
+    Y = x - t + s2;
 }
 
 // Gentleman-Sande butterfly of the inverse (R5): inputs and outputs below
-// 4p + 2^(32+s) after s stages (< 4p + 2^49 for N <= 2^17).
+// 4p + 2^(32+s) after s stages (< 4p + 2^49 for N <= 2^17): with inputs
+// below 4p + E the carry-free test below subtracts only when x + y > 4p and
+// leaves x + y < 4p + 2^33 otherwise, so E' = max(2E, 2^33).
 //   X' = (X + Y) mod* 4p;  Y' = (X - Y + 5p) w  (5p > any Y, so no wrap).
 template <class W>
 __device__ __forceinline__ void gs_bf(uint64_t& X, uint64_t& Y, const W& w, const PrimeConst& c)
 {
     const uint64_t x = X, y = Y;
-    X = csub_hi(x + y, c.p4, c.p4_hi);
+    // subtract 4p iff hi(x) + hi(y) > hi(4p): a carry-free test, so X' is
+    // one 3-input add (see ct_bf)
+    const bool ge = (uint32_t)(x >> 32) + (uint32_t)(y >> 32) > c.p4_hi;
+    X = x + y - (ge ? c.p4 : 0);
     Y = w.mul(x - y + c.p5, c);
 }
 

@@ -686,6 +686,7 @@ cudaError_t launch_pointwise(const KArgs& a, cudaStream_t st)
 }
 
 // ---------------------------------------------------------------- dispatch
+#ifndef NTT_KERNELS_ONLY  // tools/sass_probe.sh compiles the kernels alone
 namespace {
 
 // SM count of the current device, cached per device (persistent-grid sizing)
@@ -882,4 +883,5 @@ cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cud
                    : cols_switch<4, false>(key, a, rows, st, K1Pairs{});
 }
 
+#endif  // NTT_KERNELS_ONLY
 }  // namespace ntt
