@@ -49,7 +49,7 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def alu_peak():
+def alu_peak(form: str = "2n"):
     """Derived integer roof: the IMAD pipe issues 16
     lanes/clk/SMSP for IMAD and 8 for IMAD.WIDE/IMAD.HI (measured,
     profiles/r01_alu_roof.jsonl); a 64-bit Shoup butterfly needs at least
@@ -57,7 +57,8 @@ def alu_peak():
     q' = 1 WIDE + 2 HI, r = 2 WIDE + 4 IMAD -> 5 x 4 + 4 x 2 = 28 IMAD-pipe
     clk per warp-butterfly per SMSP.  148 SMs x 4 SMSP x 32 / 28 per clk."""
     sm_clk_ghz = 1.965
-    bfly_per_clk = 148 * 4 * 32 / 28.0
+    # Proth primes (p = 1 mod 2^32): r = 1 WIDE + 3 IMAD -> 4 x 4 + 3 x 2 = 22 clk
+    bfly_per_clk = 148 * 4 * 32 / (22.0 if form == "proth" else 28.0)
     return bfly_per_clk * sm_clk_ghz  # G butterflies / s
 
 
@@ -212,7 +213,7 @@ def run_own(args):
     logn, L_total, batch_per_gpu, text = CONFIGS[args.config]
     N = 1 << logn
     sh = my_shard(rank, world, L_total, batch_per_gpu)
-    all_primes = find_primes(N, L_total)
+    all_primes = find_primes(N, L_total, args.primes)
     primes = all_primes[sh["prime_offset"]: sh["prime_offset"] + sh["L"]]
     L, B = sh["L"], sh["batch"]
     words = B * L * N
@@ -283,7 +284,7 @@ def run_own(args):
         st = logn
     bfly_per_launch = rows * (N // 2) * st
     achieved = bfly_per_launch / (dom_ms * 1e-3) / 1e9
-    peak = alu_peak()
+    peak = alu_peak(args.primes if info.get("proth") else "2n")
     dom_bytes = 2 * 8 * N * rows  # compulsory bytes of one pass: read + write every word
     hbm_dom = dom_bytes / (dom_ms * 1e-3) / 1e9
     traffic = None
@@ -293,6 +294,28 @@ def run_own(args):
             traffic = json.load(open(tr_path)).get(dom)
         except Exception:
             traffic = None
+
+    # the paper's two-kernel split (two HBM passes per direction), same primes and inputs
+    tk_plan = Plan(N, primes, fused=False)
+    tk_steps = max(3, args.steps // 2)
+    ms_tk, kern_tk, _, _ = timed(tk_plan, tk_steps, 2)
+    tk_plan.close()
+
+    # the other prime family, same workload, reported beside
+    alt_form = "2n" if args.primes == "proth" else "proth"
+    alt_primes = find_primes(N, L_total, alt_form)[sh["prime_offset"]: sh["prime_offset"] + sh["L"]]
+    alt_host = torch.empty(words, dtype=torch.int64)
+    synth.rns_rows(alt_primes, B, N, config_id=cfg_id, prime_offset=sh["prime_offset"], L_total=L_total,
+                   batch_offset=sh["batch_offset"], out=alt_host.numpy().view(np.uint64).reshape(B, L, N))
+    dev.copy_(alt_host.cuda())
+    alt_plan = Plan(N, alt_primes)
+    alt_steps = max(3, args.steps // 2)
+    ms_alt, kern_alt, _, _ = timed(alt_plan, alt_steps, 2)
+    alt_ok = bool(torch.equal(dev, alt_host.cuda()))
+    alt_proth = alt_plan.info()["proth"]
+    alt_plan.close()
+    del alt_host
+    dev.copy_(host.cuda())
 
     # OT on: same workload, reported beside (north_star: OT on/off)
     ot_plan = Plan(N, primes, ot=True)
@@ -358,7 +381,10 @@ def run_own(args):
                 "workload": f"{args.config}: {text} per GPU; one step = NTT + iNTT of every row",
                 "N": N, "L": L_total, "batch_per_gpu": batch_per_gpu, "global_batch": units,
                 "shard": f"{sh['Gp']} prime ranges x {sh['Gb']} ciphertext ranges",
-                "log_n1": info["log_n1"], "ot": False,
+                "log_n1": info["log_n1"], "passes": info["passes"], "cluster": info["cluster"], "ot": False,
+                "primes": {"2n": "p = 1 mod 2N descending from 2^60 - 2N + 1 (DESIGN.md R3)",
+                           "proth": "p = 1 mod 2^32 descending from 2^60 - 2^32 + 1 (DESIGN.md 5.1)"}[args.primes],
+                "proth_arith": bool(info.get("proth")),
                 "l2": "inputs larger than L2 (%.0f MiB per GPU vs 126 MB L2)" % (words * 8 / 2**20),
             },
             "residue_ntts_per_s": round(2 * rows * world / (ms_step * 1e-3), 1),
@@ -372,6 +398,13 @@ def run_own(args):
                         "bytes": "compulsory 16N per row per pass"},
             },
             "kernels_ms": {k: round(v, 4) for k, v in kern.items()},
+            "two_kernel": {"value": round(ms_tk / tk_steps * 1e3 / units, 3), "unit": "us",
+                           "ms_per_step": round(ms_tk / tk_steps, 4),
+                           "kernels_ms": {k: round(v, 4) for k, v in kern_tk.items()}},
+            "other_primes": {"primes": alt_form, "proth_arith": alt_proth,
+                             "value": round(ms_alt / alt_steps * 1e3 / units, 3), "unit": "us",
+                             "ms_per_step": round(ms_alt / alt_steps, 4), "roundtrip_exact": alt_ok,
+                             "kernels_ms": {k: round(v, 4) for k, v in kern_alt.items()}},
             "ot_on": {"value": round(ms_ot / ot_steps * 1e3 / units, 3), "unit": "us",
                       "ms_per_step": round(ms_ot / ot_steps, 4),
                       "kernels_ms": {k: round(v, 4) for k, v in kern_ot.items()}},
@@ -399,6 +432,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
+    ap.add_argument("--primes", default="proth", choices=["2n", "proth"],
+                    help="prime family: proth = p = 1 mod 2^32 (default), 2n = DESIGN.md R3")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -55,7 +55,25 @@ typedef struct {
     unsigned ot_stages;  /* 1 or 2 (fig:3point c); 0 = 2 */
     unsigned log_n1;     /* two-kernel split N = N1*N2, log2 N1;
                             0 = automatic; ignored when one kernel holds the row */
+    int proth_arith;     /* 0 = automatic: when EVERY prime is = 1 mod 2^32 the
+                            kernels form lo64(q p) of Shoup's modmul
+                            as q + (q0 p1 << 32); -1 = always the
+                            general arithmetic.  Results are identical either way. */
+    int fused;           /* single pass per direction for N = 2^14..2^17: one
+                            thread-block cluster of N/2^13 CTAs holds the row in
+                            distributed shared memory, so each word crosses HBM
+                            once per direction instead of twice (the paper's
+                            two-kernel premise, lifted).  0 / -1 = off
+                            (the two-kernel split: measured faster on B200, where
+                            the path is bound by the multiply pipe, not HBM --
+                            DESIGN.md 5.5), 1 = on (NTT_ERR_INVALID_ARG if N is
+                            outside 2^14..2^17, OT is on or log_n1 is given). */
 } ntt_opts_t;
+
+/* Prime families for ntt_find_primes_ex. */
+#define NTT_PRIMES_2N 0u      /* p = 1 mod 2N, descending from 2^60 - 2N + 1 (R3) */
+#define NTT_PRIMES_PROTH32 1u /* p = 1 mod 2^32 (hence = 1 mod 2N for N <= 2^17),
+                                 descending from 2^60 - 2^32 + 1 */
 
 /* ntt_find_primes -- host helper, no device needed.
  * Writes the first `count` primes p = 1 (mod 2N), 2^59 <= p < 2^60, scanning
@@ -63,6 +81,17 @@ typedef struct {
  * Deterministic.  n = N (power of two, 2 <= N <= 2^17).
  * Errors: INVALID_N, INVALID_ARG (out == NULL or count == 0), RANGE_EXHAUSTED. */
 ntt_status_t ntt_find_primes(unsigned n, unsigned count, uint64_t *out);
+
+/* ntt_find_primes_ex -- as ntt_find_primes, for a prime family:
+ *   NTT_PRIMES_2N      : identical to ntt_find_primes;
+ *   NTT_PRIMES_PROTH32 : the first `count` primes p = k 2^32 + 1 in
+ *                        [2^59, 2^60), descending.  P:423 fixes only the range
+ *                        ("between 2^59 and 2^60") and p = 1 mod N (R1);
+ *                        this family meets both for every N <= 2^17 and lets
+ *                        the kernels drop one 32x32 product per modmul.
+ * out: host array of `count` uint64 (caller-owned).  Errors: INVALID_N,
+ * INVALID_ARG (null out, count 0, unknown form), RANGE_EXHAUSTED. */
+ntt_status_t ntt_find_primes_ex(unsigned n, unsigned count, unsigned form, uint64_t *out);
 
 /* ntt_find_psi -- host helper.  The smallest primitive 2N-th root of unity mod
  * p (psi^N = -1; R2) into *psi.  Errors: INVALID_N, INVALID_PRIME. */
@@ -92,6 +121,15 @@ ntt_status_t ntt_plan_psi(ntt_plan_t plan, uint64_t *psi_out);
 ntt_status_t ntt_plan_info(ntt_plan_t plan, unsigned *L, unsigned *logn, unsigned *log_n1,
                            int *ot_enable, unsigned *ot_base, unsigned *ot_stages,
                            uint64_t *table_bytes);
+
+/* ntt_plan_exec -- host query of how the plan executes (any output may be NULL):
+ * *proth   = 1 if it runs the Proth-prime arithmetic (every prime = 1 mod 2^32
+ *            and proth_arith != -1), else 0;
+ * *passes  = kernels per direction (1: single CTA or single-pass cluster
+ *            kernel; 2: the paper's two-kernel split);
+ * *cluster = CTAs per row of the single-pass cluster kernel (N / 2^13), 1 if
+ *            it is not used. */
+ntt_status_t ntt_plan_exec(ntt_plan_t plan, int *proth, unsigned *passes, unsigned *cluster);
 
 /* ntt_forward -- in-place forward merged negacyclic NTT of batch*L rows.
  *   data: DEVICE pointer on the plan's device, 16-byte aligned, to

@@ -14,16 +14,20 @@ from __future__ import annotations
 
 import ctypes
 
-from ._native import NTT_DIR_FORWARD, NTT_DIR_INVERSE, NttError, Opts, check, lib
+from ._native import NTT_DIR_FORWARD, NTT_DIR_INVERSE, NTT_PRIMES_2N, NTT_PRIMES_PROTH32, NttError, Opts, check, lib
 
 __all__ = ["Plan", "Plan32", "find_primes", "find_primes32", "find_psi", "NttError", "NTT_DIR_FORWARD",
            "NTT_DIR_INVERSE"]
 
 
-def find_primes(N: int, count: int) -> list[int]:
-    """First ``count`` primes p = 1 mod 2N in [2^59, 2^60), descending (host)."""
+PRIME_FORMS = {"2n": NTT_PRIMES_2N, "proth": NTT_PRIMES_PROTH32}
+
+
+def find_primes(N: int, count: int, form: str = "2n") -> list[int]:
+    """First ``count`` primes in [2^59, 2^60), descending (host): form "2n" =
+    p = 1 mod 2N from 2^60 - 2N + 1 (R3); "proth" = p = 1 mod 2^32."""
     out = (ctypes.c_uint64 * count)()
-    check(lib().ntt_find_primes(N, count, out), "ntt_find_primes")
+    check(lib().ntt_find_primes_ex(N, count, PRIME_FORMS[form], out), "ntt_find_primes_ex")
     return [int(v) for v in out]
 
 
@@ -72,12 +76,13 @@ class Plan:
     CUDA device (ntt_plan_create_ex)."""
 
     def __init__(self, N: int, primes, ot: bool = False, ot_base: int = 0, ot_stages: int = 0,
-                 log_n1: int = 0):
+                 log_n1: int = 0, proth_arith: bool = True, fused: bool | None = None):
         self.N = int(N)
         self.primes = [int(p) for p in primes]
         self.L = len(self.primes)
         arr = (ctypes.c_uint64 * max(self.L, 1))(*self.primes)
-        opts = Opts(1 if ot else -1, ot_base, ot_stages, log_n1)
+        opts = Opts(1 if ot else -1, ot_base, ot_stages, log_n1, 0 if proth_arith else -1,
+                    0 if fused is None else (1 if fused else -1))
         h = ctypes.c_void_p()
         check(lib().ntt_plan_create_ex(ctypes.byref(h), self.N, arr, self.L, ctypes.byref(opts)),
               "ntt_plan_create")
@@ -98,12 +103,15 @@ class Plan:
 
     def info(self) -> dict:
         L, logn, logn1, ots, otb = (ctypes.c_uint() for _ in range(5))
-        ote = ctypes.c_int()
+        ote, pr = ctypes.c_int(), ctypes.c_int()
         tb = ctypes.c_uint64()
         check(lib().ntt_plan_info(self.handle, ctypes.byref(L), ctypes.byref(logn), ctypes.byref(logn1),
                                   ctypes.byref(ote), ctypes.byref(otb), ctypes.byref(ots), ctypes.byref(tb)))
+        npass, ncl = ctypes.c_uint(), ctypes.c_uint()
+        check(lib().ntt_plan_exec(self.handle, ctypes.byref(pr), ctypes.byref(npass), ctypes.byref(ncl)))
         return {"L": L.value, "logn": logn.value, "log_n1": logn1.value, "ot_enable": bool(ote.value),
-                "ot_base": otb.value, "ot_stages": ots.value, "table_bytes": tb.value}
+                "ot_base": otb.value, "ot_stages": ots.value, "table_bytes": tb.value, "proth": bool(pr.value),
+                "passes": npass.value, "cluster": ncl.value}
 
     # ---------------------------------------------------------------- transforms
     def forward(self, x, stream=None):
@@ -121,7 +129,7 @@ class Plan:
     @property
     def passes(self) -> int:
         """Kernels per direction: 2 for the two-kernel split, 1 otherwise."""
-        return 2 if self.info()["log_n1"] else 1
+        return self.info()["passes"]
 
     def launch_pass(self, x, direction: int, pass_index: int, stream=None):
         """Enqueue one kernel of a direction (for per-kernel timing)."""

@@ -18,10 +18,11 @@ STATUS = {
 NTT_DIR_FORWARD = 1
 NTT_DIR_INVERSE = 2
 NTT_VARIANT_DEFAULT, NTT_VARIANT_RADIX2, NTT_VARIANT_RADIX16 = 0, 1, 2
+NTT_PRIMES_2N, NTT_PRIMES_PROTH32 = 0, 1
 
 # every symbol include/ntt.h declares
 EXPORTS = [
-    "ntt_find_primes", "ntt_find_psi", "ntt_plan_create", "ntt_plan_create_ex", "ntt_plan_psi",
+    "ntt_find_primes", "ntt_find_primes_ex", "ntt_plan_exec", "ntt_find_psi", "ntt_plan_create", "ntt_plan_create_ex", "ntt_plan_psi",
     "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_launch_pass", "ntt_pointwise_inverse", "ntt_negacyclic_mul", "ntt_forward_variant",
     "ntt_execute_host", "ntt_workspace_words",
     "ntt_plan_destroy", "ntt_status_string",
@@ -40,7 +41,8 @@ class NttError(RuntimeError):
 
 class Opts(ctypes.Structure):
     _fields_ = [("ot_enable", ctypes.c_int), ("ot_base", ctypes.c_uint),
-                ("ot_stages", ctypes.c_uint), ("log_n1", ctypes.c_uint)]
+                ("ot_stages", ctypes.c_uint), ("log_n1", ctypes.c_uint), ("proth_arith", ctypes.c_int),
+                ("fused", ctypes.c_int)]
 
 
 _lib = None
@@ -57,6 +59,8 @@ def lib() -> ctypes.CDLL:
         p64 = ctypes.POINTER(ctypes.c_uint64)
         pp = ctypes.POINTER(ctypes.c_void_p)
         L.ntt_find_primes.argtypes = [u32, u32, p64]
+        L.ntt_find_primes_ex.argtypes = [u32, u32, u32, p64]
+        L.ntt_plan_exec.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(u32), ctypes.POINTER(u32)]
         L.ntt_find_psi.argtypes = [u64, u32, p64]
         L.ntt_plan_create.argtypes = [pp, u32, p64, u32]
         L.ntt_plan_create_ex.argtypes = [pp, u32, p64, u32, ctypes.POINTER(Opts)]
@@ -82,7 +86,7 @@ def lib() -> ctypes.CDLL:
         L.ntt_plan_destroy32.argtypes = [vp]
         L.ntt_status_string.argtypes = [i32]
         L.ntt_status_string.restype = ctypes.c_char_p
-        for name in ["ntt_find_primes", "ntt_find_psi", "ntt_plan_create", "ntt_plan_create_ex",
+        for name in ["ntt_find_primes", "ntt_find_primes_ex", "ntt_plan_exec", "ntt_find_psi", "ntt_plan_create", "ntt_plan_create_ex",
                      "ntt_plan_psi", "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_launch_pass", "ntt_forward_variant",
                      "ntt_pointwise_inverse", "ntt_negacyclic_mul", "ntt_execute_host",
                      "ntt_plan_destroy", "ntt_find_primes32", "ntt_plan_create32", "ntt_plan_info32",

@@ -34,6 +34,8 @@ struct ntt_plan_s {
     PrimeConst* d_pc_mont = nullptr;  // [L] the same with N^-1 scaled by 2^64 (NTT-domain products)
     uint64_t table_bytes = 0;
     int loge_k1 = 4, loge_k2 = 5;  // Kernel-1 radix exponent; Kernel-2 variant (5 = pipelined radix-16)
+    bool proth = false;            // every prime = 1 mod 2^32: PrimeConstP kernels
+    bool fused = false;            // single-pass cluster kernel per direction (log_n1 = log2 cluster size)
 };
 
 namespace {
@@ -125,6 +127,34 @@ KArgs base_args(const ntt_plan_s* plan, uint64_t* data, unsigned batch, bool inv
     return a;
 }
 
+// The two kernels of one direction over `rows` rows of `a` (pass < 0: both).
+cudaError_t two_pass(const ntt_plan_s* plan, KArgs a, uint32_t rows, bool inverse, int ots, int pass, cudaStream_t st)
+{
+    a.total_blocks = rows << plan->log_n1;
+    a.log_tiles = plan->logn - plan->log_n1 - 4;
+    cudaError_t e = cudaSuccess;
+    if (!inverse) {
+        if (pass != 1 && (e = ntt::launch_k1(false, plan->loge_k1, a, rows, st, plan->proth)) != cudaSuccess)
+            return e;
+        if (pass != 0) e = ntt::launch_k2(false, plan->loge_k2, a, ots, 1, st, plan->proth);
+        return e;
+    }
+    if (pass != 1) {
+        e = ntt::launch_k2(true, plan->loge_k2, a, ots, 1, st, plan->proth);
+        if (e == cudaErrorNotSupported && a.mul_a) {  // unfused: product kernel, then Kernel-2'
+            cudaGetLastError();
+            if ((e = ntt::launch_pointwise(a, st)) != cudaSuccess) return e;
+            KArgs b = a;
+            b.mul_a = nullptr;
+            e = ntt::launch_k2(true, plan->loge_k2, b, ots, 1, st, plan->proth);
+        }
+        if (e != cudaSuccess) return e;
+    }
+    a.mul_a = nullptr;
+    if (pass != 0) e = ntt::launch_k1(true, plan->loge_k1, a, rows, st, plan->proth);
+    return e;
+}
+
 // Enqueue one direction (pass < 0: all passes) on `st`; no checks.  mul_a:
 // fuse data <- mul_a (.) data into the inverse's first kernel (Montgomery,
 // with the R-scaled N^-1 constants).
@@ -138,39 +168,26 @@ cudaError_t enqueue(const ntt_plan_s* plan, uint64_t* data, unsigned batch, bool
     }
     const uint32_t rows = batch * plan->L;
     const int ots = plan->ot_enable ? (int)plan->ot_stages : 0;
+    if (plan->fused) {
+        if (mul_a) {  // the product is not fused into the cluster kernel: element-wise kernel first
+            cudaError_t e = ntt::launch_pointwise(a, st);
+            if (e != cudaSuccess) return e;
+            a.mul_a = nullptr;
+        }
+        return ntt::launch_fused(inverse, a, rows, st, plan->proth);
+    }
     if (plan->log_n1 == 0) {
         a.total_blocks = rows;
-        cudaError_t e = ntt::launch_single(inverse, a, ots, 1, st);
+        cudaError_t e = ntt::launch_single(inverse, a, ots, 1, st, plan->proth);
         if (e == cudaErrorNotSupported && mul_a) {  // unfused: product kernel, then the inverse
             cudaGetLastError();
             if ((e = ntt::launch_pointwise(a, st)) != cudaSuccess) return e;
             a.mul_a = nullptr;
-            e = ntt::launch_single(inverse, a, ots, 1, st);
+            e = ntt::launch_single(inverse, a, ots, 1, st, plan->proth);
         }
         return e;
     }
-    a.total_blocks = rows << plan->log_n1;
-    a.log_tiles = plan->logn - plan->log_n1 - 4;
-    cudaError_t e = cudaSuccess;
-    if (!inverse) {
-        if (pass != 1 && (e = ntt::launch_k1(false, plan->loge_k1, a, rows, st)) != cudaSuccess) return e;
-        if (pass != 0) e = ntt::launch_k2(false, plan->loge_k2, a, ots, 1, st);
-        return e;
-    }
-    if (pass != 1) {
-        e = ntt::launch_k2(true, plan->loge_k2, a, ots, 1, st);
-        if (e == cudaErrorNotSupported && mul_a) {  // unfused: product kernel, then Kernel-2'
-            cudaGetLastError();
-            if ((e = ntt::launch_pointwise(a, st)) != cudaSuccess) return e;
-            KArgs b = a;
-            b.mul_a = nullptr;
-            e = ntt::launch_k2(true, plan->loge_k2, b, ots, 1, st);
-        }
-        if (e != cudaSuccess) return e;
-    }
-    a.mul_a = nullptr;
-    if (pass != 0) e = ntt::launch_k1(true, plan->loge_k1, a, rows, st);
-    return e;
+    return two_pass(plan, a, rows, inverse, ots, pass, st);
 }
 
 ntt_status_t run(ntt_plan_t plan, uint64_t* data, unsigned batch, void* stream, bool inverse, int pass = -1)
@@ -210,6 +227,18 @@ ntt_status_t ntt_find_primes(unsigned n, unsigned count, uint64_t* out)
     if (!out || count == 0) return NTT_ERR_INVALID_ARG;
     std::vector<uint64_t> v;
     if (!nttp::ntt_primes(n, count, v)) return NTT_ERR_RANGE_EXHAUSTED;
+    std::copy(v.begin(), v.end(), out);
+    return NTT_OK;
+}
+
+ntt_status_t ntt_find_primes_ex(unsigned n, unsigned count, unsigned form, uint64_t* out)
+{
+    if (form == NTT_PRIMES_2N) return ntt_find_primes(n, count, out);
+    if (form != NTT_PRIMES_PROTH32) return NTT_ERR_INVALID_ARG;
+    if (!pow2_in(n, 1, 17)) return NTT_ERR_INVALID_N;
+    if (!out || count == 0) return NTT_ERR_INVALID_ARG;
+    std::vector<uint64_t> v;
+    if (!nttp::proth_primes(count, v)) return NTT_ERR_RANGE_EXHAUSTED;
     std::copy(v.begin(), v.end(), out);
     return NTT_OK;
 }
@@ -266,6 +295,15 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
     if (ot_stages > 2) return NTT_ERR_INVALID_ARG;
     const unsigned last_kernel_stages = log_n1 ? logn - log_n1 : logn;
     if (ot_stages > last_kernel_stages) ot_stages = last_kernel_stages;
+    if (opts.proth_arith < -1 || opts.proth_arith > 0) return NTT_ERR_INVALID_ARG;
+    if (opts.fused < -1 || opts.fused > 1) return NTT_ERR_INVALID_ARG;
+    // single pass per direction (cluster kernel): N = 2^14..2^17, no OT, no explicit split
+    const bool fused_ok = logn >= 14 && logn <= 17 && !ot_enable && opts.log_n1 == 0;
+    if (opts.fused == 1 && !fused_ok) return NTT_ERR_INVALID_ARG;
+    const bool fused = fused_ok && opts.fused == 1;
+    if (fused) log_n1 = logn - 13;
+    bool all_proth = opts.proth_arith == 0;
+    for (unsigned i = 0; i < L; ++i) all_proth = all_proth && (uint32_t)pr[i] == 1u;
 
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) {
@@ -298,6 +336,9 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
             p->loge_k2 = a2;
         }
     }
+    // the Proth kernels exist for the default variants only (ntt_kernels.cuh)
+    p->proth = all_proth && (((p->loge_k1 == 4 || p->loge_k1 == 5) && p->loge_k2 == 5) || fused);
+    p->fused = fused;
 
     // host tables, one thread per hardware thread over primes
     const uint64_t N = n, NOT = ot_base + N / ot_base;
@@ -330,7 +371,8 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
                 uint64_t inv = 1;  // p^-1 mod 2^64 by Newton iteration (p odd)
                 for (int it = 0; it < 6; ++it) inv *= 2 - q * inv;
                 c.pinv = 0 - inv;
-                c.pad2 = 0;
+                c.m1 = 0u - (uint32_t)(q >> 32);
+                c.proth = (uint32_t)q == 1u;
                 nttp::Twiddle t1 = nttp::shoup_pair(ninv, q), t2 = nttp::shoup_pair(ninv_psi, q);
                 c.ninv = Tw{t1.w, t1.wb};
                 c.ninv_psi = Tw{t2.w, t2.wb};
@@ -351,7 +393,7 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
     const bool k2tab = log_n1 != 0;
     std::vector<Tw> h_fwd2, h_inv2;
     if (k2tab) {
-        const unsigned loge = (p->loge_k2 == 3 || p->loge_k2 == 6) ? 3 : 4;
+        const unsigned loge = (!fused && (p->loge_k2 == 3 || p->loge_k2 == 6)) ? 3 : 4;
         h_fwd2.resize(N * L);
         h_inv2.resize(N * L);
         std::vector<std::thread> th2;
@@ -414,6 +456,15 @@ ntt_status_t ntt_plan_info(ntt_plan_t plan, unsigned* L, unsigned* logn, unsigne
     return NTT_OK;
 }
 
+ntt_status_t ntt_plan_exec(ntt_plan_t plan, int* proth, unsigned* passes, unsigned* cluster)
+{
+    if (!plan) return NTT_ERR_INVALID_ARG;
+    if (proth) *proth = plan->proth ? 1 : 0;
+    if (passes) *passes = (plan->fused || plan->log_n1 == 0) ? 1u : 2u;
+    if (cluster) *cluster = plan->fused ? (1u << plan->log_n1) : 1u;
+    return NTT_OK;
+}
+
 ntt_status_t ntt_forward(ntt_plan_t plan, uint64_t* data, unsigned batch, void* stream)
 {
     return run(plan, data, batch, stream, false);
@@ -428,8 +479,9 @@ ntt_status_t ntt_launch_pass(ntt_plan_t plan, uint64_t* data, unsigned batch, un
                              void* stream)
 {
     if (!plan || (dir != NTT_DIR_FORWARD && dir != NTT_DIR_INVERSE)) return NTT_ERR_INVALID_ARG;
-    if (pass > 1 || (pass == 1 && plan->log_n1 == 0)) return NTT_ERR_INVALID_ARG;
-    return run(plan, data, batch, stream, dir == NTT_DIR_INVERSE, plan->log_n1 == 0 ? -1 : (int)pass);
+    const bool one = plan->fused || plan->log_n1 == 0;
+    if (pass > 1 || (pass == 1 && one)) return NTT_ERR_INVALID_ARG;
+    return run(plan, data, batch, stream, dir == NTT_DIR_INVERSE, one ? -1 : (int)pass);
 }
 
 ntt_status_t ntt_pointwise_inverse(ntt_plan_t plan, const uint64_t* a_ntt, uint64_t* data, unsigned batch,

@@ -26,8 +26,25 @@ struct __align__(16) PrimeConst {
     Tw ninv;             // N^-1   [R-scaled copy: N^-1 2^64, see mont_mul]
     Tw ninv_psi;         // N^-1 * Psi^-1[1], the fused last GS stage (R15)
     uint64_t pinv;       // -p^-1 mod 2^64 (Montgomery, NTT-domain products)
-    uint64_t pad2;
+    uint32_t m1;         // 2^32 - (p >> 32): the Proth form below
+    uint32_t proth;      // 1 if p = 1 mod 2^32 (set by the plan)
 };
+
+// The same constants, as a type that selects the Proth-prime arithmetic: for
+// p = p1 2^32 + 1 (p = 1 mod 2^32) the low 64 bits of
+// q p are q + (q0 p1 << 32), one IMAD instead of an IMAD.WIDE and two IMADs.
+// Kernels templated on PrimeConstP are launched only for plans whose primes
+// all have this form (ntt_api.cu).
+struct PrimeConstP : PrimeConst {
+};
+
+template <class C>
+__device__ __forceinline__ C load_pc(const PrimeConst* pc, uint32_t l)
+{
+    C c;
+    static_cast<PrimeConst&>(c) = pc[l];
+    return c;
+}
 
 // Kernel arguments (passed by value, lives in the constant bank).
 struct KArgs {
@@ -108,6 +125,50 @@ __device__ __forceinline__ uint64_t shoup_lazy(uint64_t b, uint64_t w, uint64_t 
     return r;
 }
 
+// Shoup's modmul for a Proth prime p = p1 2^32 + 1: the same truncated
+// quotient q' (so the same [0, 4p) output bound), and
+//   r = b w - q' p = lo64(b w) - q' - (q0' p1 << 32)  (mod 2^64),
+// formed as one IMAD.WIDE b0 w0 with the addend -q' plus three IMADs into the
+// high word (m1 = -p1 mod 2^32): 2 IMAD.WIDE, 2 IMAD.HI and 3 IMAD in all.
+__device__ __forceinline__ uint64_t shoup_lazy_p(uint64_t b, uint64_t w, uint64_t wb, uint32_t m1)
+{
+    uint64_t r;
+    asm("{\n\t"
+        ".reg .u32 b0, b1, v0, v1, w0, w1, t0, t1, q0, q1, r0, r1;\n\t"
+        ".reg .u64 q, a, t;\n\t"
+        "mov.b64 {b0, b1}, %1;\n\t"
+        "mov.b64 {w0, w1}, %2;\n\t"
+        "mov.b64 {v0, v1}, %3;\n\t"
+        "mul.hi.u32 t0, b1, v0;\n\t"
+        "mul.hi.u32 t1, b0, v1;\n\t"
+        "cvt.u64.u32 t, t0;\n\t"
+        "mad.wide.u32 q, b1, v1, t;\n\t"
+        "cvt.u64.u32 t, t1;\n\t"
+        "add.u64 q, q, t;\n\t"
+        "mov.b64 {q0, q1}, q;\n\t"
+        "sub.u64 q, 0, q;\n\t"
+        "mad.wide.u32 a, b0, w0, q;\n\t"
+        "mov.b64 {r0, r1}, a;\n\t"
+        "mad.lo.u32 r1, b0, w1, r1;\n\t"
+        "mad.lo.u32 r1, b1, w0, r1;\n\t"
+        "mad.lo.u32 r1, q0, %4, r1;\n\t"
+        "mov.b64 %0, {r0, r1};\n\t"
+        "}"
+        : "=l"(r)
+        : "l"(b), "l"(w), "l"(wb), "r"(m1));
+    return r;
+}
+
+// One Shoup multiply by a table twiddle, arithmetic chosen by the constants' type.
+__device__ __forceinline__ uint64_t shoup(uint64_t b, const Tw& t, const PrimeConst& c)
+{
+    return shoup_lazy(b, t.w, t.wb, c.np);
+}
+__device__ __forceinline__ uint64_t shoup(uint64_t b, const Tw& t, const PrimeConstP& c)
+{
+    return shoup_lazy_p(b, t.w, t.wb, c.m1);
+}
+
 __device__ __forceinline__ uint64_t csub(uint64_t x, uint64_t m) { return x >= m ? x - m : x; }
 
 // Element-wise product of two NTT-domain operands (the odot) --
@@ -139,25 +200,27 @@ struct TwMul;
 template <>
 struct TwMul<false> {
     Tw t;
-    __device__ __forceinline__ uint64_t mul(uint64_t x, const PrimeConst& c) const
+    template <class C>
+    __device__ __forceinline__ uint64_t mul(uint64_t x, const C& c) const
     {
-        return shoup_lazy(x, t.w, t.wb, c.np);
+        return shoup(x, t, c);
     }
 };
 template <>
 struct TwMul<true> {
     Tw fine, coarse;
-    __device__ __forceinline__ uint64_t mul(uint64_t x, const PrimeConst& c) const
+    template <class C>
+    __device__ __forceinline__ uint64_t mul(uint64_t x, const C& c) const
     {
-        return shoup_lazy(shoup_lazy(x, fine.w, fine.wb, c.np), coarse.w, coarse.wb, c.np);
+        return shoup(shoup(x, fine, c), coarse, c);
     }
 };
 
 // Cooley-Tukey butterfly (Algorithm 2) in Harvey's lazy form (R9),
 // widened for the [0,4p) multiplier: inputs and outputs in [0, 8p + 2^32).
 //   X <- X mod* 4p (< 4p + 2^32);  T = Y w (< 4p);  X' = X + T;  Y' = X - T + 4p.
-template <class W>
-__device__ __forceinline__ void ct_bf(uint64_t& X, uint64_t& Y, const W& w, const PrimeConst& c)
+template <class W, class C>
+__device__ __forceinline__ void ct_bf(uint64_t& X, uint64_t& Y, const W& w, const C& c)
 {
     // the conditional subtraction folded into both outputs as 3-input adds
     // (IADD3 / IADD3.X on the ALU pipe; a 2-input 64-bit add lets ptxas emit
@@ -175,8 +238,8 @@ __device__ __forceinline__ void ct_bf(uint64_t& X, uint64_t& Y, const W& w, cons
 // below 4p + E the carry-free test below subtracts only when x + y > 4p and
 // leaves x + y < 4p + 2^33 otherwise, so E' = max(2E, 2^33).
 //   X' = (X + Y) mod* 4p;  Y' = (X - Y + 5p) w  (5p > any Y, so no wrap).
-template <class W>
-__device__ __forceinline__ void gs_bf(uint64_t& X, uint64_t& Y, const W& w, const PrimeConst& c)
+template <class W, class C>
+__device__ __forceinline__ void gs_bf(uint64_t& X, uint64_t& Y, const W& w, const C& c)
 {
     const uint64_t x = X, y = Y;
     // subtract 4p iff hi(x) + hi(y) > hi(4p): a carry-free test, so X' is
@@ -280,9 +343,9 @@ struct TwKey {
 // NI sub-transforms per thread share every twiddle (Kernel-1 columns of one
 // tile; Kernel-2 blocks of one prime at the same block position): one twiddle
 // load serves NI times the butterflies, and NI independent chains add ILP.
-template <int LOGM, int LOGE, int RI, int OT_FROM, int NI, class TabF, class OtF>
+template <int LOGM, int LOGE, int RI, int OT_FROM, int NI, class TabF, class OtF, class C>
 __device__ __forceinline__ void ct_roundN(uint64_t (&x)[NI][16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
-                                          const OtF& otf, const PrimeConst& c)
+                                          const OtF& otf, const C& c)
 {
     using Geo = RoundGeo<LOGM, RI, LOGE>;
     constexpr int R = Geo::R, S = Geo::S;
@@ -314,9 +377,9 @@ __device__ __forceinline__ void ct_roundN(uint64_t (&x)[NI][16], uint32_t tib, u
     }
 }
 
-template <int LOGM, int LOGE, int RI, int OT_FROM, class TabF, class OtF>
+template <int LOGM, int LOGE, int RI, int OT_FROM, class TabF, class OtF, class C>
 __device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
-                                         const OtF& otf, const PrimeConst& c)
+                                         const OtF& otf, const C& c)
 {
     ct_roundN<LOGM, LOGE, RI, OT_FROM, 1>(reinterpret_cast<uint64_t(&)[1][16]>(x), tib, Fm1, tabf, otf, c);
 }
@@ -324,9 +387,9 @@ __device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32
 // Inverse round: the same groups and twiddle indices, Gentleman-Sande stages
 // in reverse order.  FUSE0: local stage 0 is global stage 0 (m = 1), where
 // N^-1 is fused: X' = (X+Y) N^-1, Y' = (X-Y) Psi^-1[1] N^-1 (R15).
-template <int LOGM, int LOGE, int RI, int OT_FROM, bool FUSE0, int NI, class TabF, class OtF>
+template <int LOGM, int LOGE, int RI, int OT_FROM, bool FUSE0, int NI, class TabF, class OtF, class C>
 __device__ __forceinline__ void gs_roundN(uint64_t (&x)[NI][16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
-                                          const OtF& otf, const PrimeConst& c)
+                                          const OtF& otf, const C& c)
 {
     using Geo = RoundGeo<LOGM, RI, LOGE>;
     constexpr int R = Geo::R, S = Geo::S;
@@ -371,9 +434,9 @@ __device__ __forceinline__ void gs_roundN(uint64_t (&x)[NI][16], uint32_t tib, u
 }
 
 // Inverse round, one sub-transform per thread.
-template <int LOGM, int LOGE, int RI, int OT_FROM, bool FUSE0, class TabF, class OtF>
+template <int LOGM, int LOGE, int RI, int OT_FROM, bool FUSE0, class TabF, class OtF, class C>
 __device__ __forceinline__ void gs_round(uint64_t (&x)[16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
-                                         const OtF& otf, const PrimeConst& c)
+                                         const OtF& otf, const C& c)
 {
     gs_roundN<LOGM, LOGE, RI, OT_FROM, FUSE0, 1>(reinterpret_cast<uint64_t(&)[1][16]>(x), tib, Fm1, tabf, otf, c);
 }

@@ -1,665 +1,9 @@
-// ntt_kernels.cu -- the sm_100a kernels of the batched negacyclic NTT / iNTT.
-//
-//   k_cols   : Kernel-1 (forward) / Kernel-1' (inverse) of the two-kernel
-//              split N = N1 * N2: the N1-point column transforms
-//              over stride-N2 columns, a 16-column tile per CTA so every global
-//              access is a full 128-byte row segment (coalescing),
-//              twiddles Psi[0..N1) preloaded into SMEM.
-//   k_contig : Kernel-2 / Kernel-2' -- contiguous N2-point blocks -- and the
-//              single-kernel path for N <= 2^13, where one CTA holds whole rows.
-//              Optional on-the-fly twiddling on the last (forward)
-//              or first (inverse) 1-2 stages.
-//
-// Both run per-thread radix-2^LOGE register NTTs with SMEM exchanges between
-// rounds; 64-bit words, Shoup modmul.
-#include "ntt_device.cuh"
-#include "ntt_launch.h"
-
-#include <algorithm>
-#include <atomic>
+// ntt_kernels.cu -- general-prime instantiation of the kernels in
+// ntt_kernels.cuh, the public launchers (which route Proth-prime plans to
+// ntt_kernels_p.cu) and the element-wise product kernel.
+#include "ntt_kernels.cuh"
 
 namespace ntt {
-
-// 16-byte asynchronous global -> shared copy (LDGSTS), and its completion.
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
-{
-    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-// ---------------------------------------------------------------- Kernel-1
-template <int LOGN1, int LOGE>
-struct ColsCfg {
-    using SC = Sched<LOGN1, LOGE>;
-    static constexpr int CT = SC::TB * 16;  // threads: 16 columns x TB per column
-    static constexpr int MINB = CT <= 256 ? 4 : (CT <= 512 ? 2 : 1);
-    static constexpr size_t SMEM = (size_t)SC::M * 16 * 8 + (size_t)SC::M * sizeof(Tw);
-};
-
-template <int LOGN1, int LOGN, int LOGE, bool INV>
-__global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>::MINB) k_cols(const KArgs a)
-{
-    using SC = Sched<LOGN1, LOGE>;
-    constexpr int M = SC::M, NR = SC::NR, CT = ColsCfg<LOGN1, LOGE>::CT;
-    extern __shared__ __align__(16) uint64_t sm[];  // [M][16] words, then Tw[M]
-    Tw* tws = reinterpret_cast<Tw*>(sm + M * 16);
-
-    const uint32_t tid = threadIdx.x, c = tid & 15u, tib = tid >> 4;
-    const uint32_t tile = blockIdx.x & ((1u << a.log_tiles) - 1u);
-    const uint32_t q = blockIdx.x >> a.log_tiles;  // prime-major: q = l * batch + b
-    const uint32_t l = q / a.batch, b = q - l * a.batch;
-    constexpr uint32_t logn2 = LOGN - LOGN1;  // compile-time stride: immediate offsets
-    uint64_t* col = a.data + (((uint64_t)b * a.L + l) << LOGN) + tile * 16u + c;
-    const Tw* tab = a.tab + ((uint64_t)l << LOGN);
-    const PrimeConst pc = a.pc[l];
-
-    for (uint32_t i = tid; i < (uint32_t)M; i += CT) tws[i] = ldg_tw(tab + i);  // Psi[0..N1)
-    __syncthreads();
-    auto tabf = [&](const TwKey& k) { return tws[k.idx]; };
-    auto otf = [&](uint32_t) { return TwMul<true>{}; };  // OT never reaches Kernel-1
-
-    uint64_t x[16];
-    // element e_k = e_0 + k s: one base address per group, compile-time offsets for k
-    auto g_load = [&](auto ri) {
-        using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
-#pragma unroll
-        for (int qd = 0; qd < Geo::GPT; ++qd) {
-            const uint64_t* p = col + ((uint64_t)Geo::elem(qd * SC::TB + tib, 0) << logn2);
-#pragma unroll
-            for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = p[(size_t)(k * Geo::s) << logn2];
-        }
-    };
-    auto g_store = [&](auto ri) {
-        using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
-#pragma unroll
-        for (int qd = 0; qd < Geo::GPT; ++qd) {
-            uint64_t* p = col + ((uint64_t)Geo::elem(qd * SC::TB + tib, 0) << logn2);
-#pragma unroll
-            for (int k = 0; k < Geo::R; ++k) p[(size_t)(k * Geo::s) << logn2] = x[qd * Geo::R + k];
-        }
-    };
-    auto s_load = [&](auto ri) {
-        using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
-#pragma unroll
-        for (int qd = 0; qd < Geo::GPT; ++qd) {
-            const uint64_t* p = sm + Geo::elem(qd * SC::TB + tib, 0) * 16 + c;
-#pragma unroll
-            for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = p[k * Geo::s * 16];
-        }
-    };
-    auto s_store = [&](auto ri) {
-        using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
-#pragma unroll
-        for (int qd = 0; qd < Geo::GPT; ++qd) {
-            uint64_t* p = sm + Geo::elem(qd * SC::TB + tib, 0) * 16 + c;
-#pragma unroll
-            for (int k = 0; k < Geo::R; ++k) p[k * Geo::s * 16] = x[qd * Geo::R + k];
-        }
-    };
-
-    if constexpr (!INV) {
-        static_for<NR>([&](auto ri) {
-            constexpr int RI = decltype(ri)::value;
-            if constexpr (RI == 0) {
-                g_load(ri);
-            } else {
-                s_load(ri);
-            }
-            ct_round<LOGN1, LOGE, RI, 1 << 20>(x, tib, 0u, tabf, otf, pc);
-            if constexpr (RI == NR - 1) {
-                g_store(ri);  // [0, 8p): Kernel-2 continues the lazy chain
-            } else {
-                s_store(ri);
-                __syncthreads();
-            }
-        });
-    } else {
-        static_for<NR>([&](auto rj) {
-            constexpr int RI = NR - 1 - decltype(rj)::value;
-            using RC = std::integral_constant<int, RI>;
-            if constexpr (RI == NR - 1) {
-                g_load(RC{});
-            } else {
-                s_load(RC{});
-            }
-            gs_round<LOGN1, LOGE, RI, 1 << 20, true>(x, tib, 0u, tabf, otf, pc);
-            if constexpr (RI == 0) {
-#pragma unroll
-                for (int k = 0; k < SC::E; ++k) x[k] = norm4(x[k], pc);  // canonical [0, p)
-                g_store(RC{});
-            } else {
-                s_store(RC{});
-                __syncthreads();
-            }
-        });
-    }
-}
-
-// ---------------------------------------------------------------- Kernel-1, pipelined
-// Persistent Kernel-1 / Kernel-1': each CTA walks the (row, 16-column tile)
-// pairs prime-major in a grid-stride loop and prefetches the next tile --
-// N1 x 128-byte row segments and the Psi[0..N1) prefix of its prime -- into
-// the other half of a double buffer with cp.async while it transforms the
-// current one.  Round 0 then reads SMEM; the last round stores straight to
-// global (whole 128-byte segments).
-template <int LOGN1, int LOGE>
-struct ColsPipeCfg {
-    using SC = Sched<LOGN1, LOGE>;
-    static constexpr int CT = SC::TB * 16;
-    static constexpr size_t BUF = (size_t)SC::M * 16 * 8 + (size_t)SC::M * sizeof(Tw);  // tile + twiddles
-    static constexpr size_t SMEM = 2 * BUF;
-    static constexpr int MINB = CT <= 256 ? 3 : 1;
-};
-
-template <int LOGN1, int LOGN, int LOGE, bool INV>
-__global__ void __launch_bounds__(ColsPipeCfg<LOGN1, LOGE>::CT, ColsPipeCfg<LOGN1, LOGE>::MINB)
-    k_cols_pipe(const KArgs a)
-{
-    using SC = Sched<LOGN1, LOGE>;
-    using CC = ColsPipeCfg<LOGN1, LOGE>;
-    constexpr int M = SC::M, NR = SC::NR, CT = CC::CT;
-    constexpr uint32_t logn2 = LOGN - LOGN1;
-    extern __shared__ __align__(16) uint64_t sm[];
-    auto tile_of = [&](uint32_t buf) { return sm + buf * (CC::BUF / 8); };
-    auto tw_of = [&](uint32_t buf) { return reinterpret_cast<Tw*>(sm + buf * (CC::BUF / 8) + M * 16); };
-
-    const uint32_t tid = threadIdx.x, c = tid & 15u, tib = tid >> 4;
-    const uint32_t tiles_per_row = 1u << a.log_tiles;
-    const uint32_t total = a.batch * a.L * tiles_per_row;
-
-    auto locate = [&](uint32_t t, uint32_t& l, uint64_t*& base) {
-        const uint32_t tile = t & (tiles_per_row - 1u), q = t >> a.log_tiles;  // q = l * batch + b
-        l = q / a.batch;
-        const uint32_t b = q - l * a.batch;
-        base = a.data + (((uint64_t)b * a.L + l) << LOGN) + tile * 16u;
-    };
-    auto prefetch = [&](uint32_t t, uint32_t buf) {
-        if (t < total) {
-            uint32_t l;
-            uint64_t* base;
-            locate(t, l, base);
-            uint64_t* st = tile_of(buf);
-            // M rows x 8 chunks of 16 bytes; thread tid takes chunks tid, tid+CT, ...
-#pragma unroll
-            for (int j = 0; j < (M * 8) / CT; ++j) {
-                const uint32_t ch = j * CT + tid, row = ch >> 3, col2 = (ch & 7u) * 2;
-                cp_async16(st + row * 16 + col2, base + ((uint64_t)row << logn2) + col2);
-            }
-            const Tw* tab = a.tab + ((uint64_t)l << LOGN);
-            Tw* tw = tw_of(buf);
-            for (uint32_t i = tid; i < (uint32_t)M; i += CT) cp_async16(tw + i, tab + i);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-
-    uint32_t t = blockIdx.x;
-    prefetch(t, 0);
-    for (uint32_t it = 0; t < total; ++it, t += gridDim.x) {
-        const uint32_t buf = it & 1u;
-        prefetch(t + gridDim.x, buf ^ 1u);
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        __syncthreads();
-
-        uint32_t l;
-        uint64_t* base;
-        locate(t, l, base);
-        uint64_t* col = base + c;
-        uint64_t* smt = tile_of(buf);
-        const Tw* tws = tw_of(buf);
-        const PrimeConst pc = a.pc[l];
-        auto tabf = [&](const TwKey& k) { return tws[k.idx]; };
-        auto otf = [&](uint32_t) { return TwMul<true>{}; };
-
-        uint64_t x[16];
-        auto g_store = [&](auto ri) {
-            using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
-#pragma unroll
-            for (int qd = 0; qd < Geo::GPT; ++qd)
-#pragma unroll
-                for (int k = 0; k < Geo::R; ++k)
-                    col[(uint64_t)Geo::elem(qd * SC::TB + tib, k) << logn2] = x[qd * Geo::R + k];
-        };
-        auto s_load = [&](auto ri) {
-            using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
-#pragma unroll
-            for (int qd = 0; qd < Geo::GPT; ++qd)
-#pragma unroll
-                for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = smt[Geo::elem(qd * SC::TB + tib, k) * 16 + c];
-        };
-        auto s_store = [&](auto ri) {
-            using Geo = RoundGeo<LOGN1, decltype(ri)::value, LOGE>;
-#pragma unroll
-            for (int qd = 0; qd < Geo::GPT; ++qd)
-#pragma unroll
-                for (int k = 0; k < Geo::R; ++k) smt[Geo::elem(qd * SC::TB + tib, k) * 16 + c] = x[qd * Geo::R + k];
-        };
-
-        if constexpr (!INV) {
-            static_for<NR>([&](auto ri) {
-                constexpr int RI = decltype(ri)::value;
-                s_load(ri);
-                ct_round<LOGN1, LOGE, RI, 1 << 20>(x, tib, 0u, tabf, otf, pc);
-                if constexpr (RI == NR - 1) {
-                    g_store(ri);
-                } else {
-                    s_store(ri);
-                    __syncthreads();
-                }
-            });
-        } else {
-            static_for<NR>([&](auto rj) {
-                constexpr int RI = NR - 1 - decltype(rj)::value;
-                using RC = std::integral_constant<int, RI>;
-                s_load(RC{});
-                gs_round<LOGN1, LOGE, RI, 1 << 20, true>(x, tib, 0u, tabf, otf, pc);
-                if constexpr (RI == 0) {
-#pragma unroll
-                    for (int k = 0; k < SC::E; ++k) x[k] = norm4(x[k], pc);
-                    g_store(RC{});
-                } else {
-                    s_store(RC{});
-                    __syncthreads();
-                }
-            });
-        }
-        __syncthreads();  // this buffer is refilled by the prefetch two iterations on
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
-// ---------------------------------------------------------------- contiguous
-template <int LOGM, int LOGE, bool TWS = false>
-struct ContigCfg {
-    static constexpr int TB = Sched<LOGM, LOGE>::TB;
-    static constexpr int CT = TB > 256 ? TB : 256;  // threads per CTA
-    static constexpr int NB = CT / TB;              // blocks per CTA iteration
-    static constexpr size_t SMEM = (size_t)NB * (1 << LOGM) * 8;  // data words
-    // register budget: the Kernel-2 mode (TWS) targets 32 warps/SM like Kernel-1
-    static constexpr int MINB = CT > 256 ? 1 : (TWS ? 3 : (LOGE >= 4 ? 2 : 3));
-};
-
-
-
-// Barrier over the TB threads of one block: blocks never share SMEM, so a
-// block that fits one warp synchronises with __syncwarp and larger blocks with
-// a named barrier of their own; CTA-wide barriers are avoided.
-template <int TB>
-__device__ __forceinline__ void block_sync(uint32_t blk)
-{
-    if constexpr (TB <= 32) {
-        __syncwarp();
-    } else {
-        asm volatile("bar.sync %0, %1;" ::"r"(blk + 1), "n"(TB) : "memory");
-    }
-}
-
-// TWS: stage each block's twiddles in SMEM.  Block bb of Kernel-2 (F = N1+bb)
-// uses Psi[F 2^j + h], h < 2^j, at local stage j: M-1 entries in log M
-// contiguous table ranges, copied with cp.async into a local table
-// tl[2^j + h] at the block's start (one latency per block instead of one per
-// round) and read back with LDS.128.  Stages under OT skip their ranges.
-template <int LOGM, int LOGE, bool INV, bool FUSE0, int OTS, bool TWS, bool MUL = false>
-__global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM, LOGE, TWS>::MINB)
-    k_contig(const KArgs a)
-{
-    using SC = Sched<LOGM, LOGE>;
-    using CC = ContigCfg<LOGM, LOGE, TWS>;
-    constexpr int M = SC::M, E = SC::E, TB = SC::TB, NR = SC::NR;
-    constexpr int OT_FROM = OTS ? LOGM - OTS : (1 << 20);
-    extern __shared__ __align__(16) uint64_t sm[];
-
-    const uint32_t tid = threadIdx.x, blk = tid / TB, tib = tid % TB;
-    uint64_t* sb = sm + blk * M;
-    const uint32_t n1mask = (1u << a.log_n1) - 1u;
-    const uint32_t B_ot = 1u << a.ot_logb;
-
-    for (uint32_t it = 0; it < a.iters; ++it) {
-        uint32_t gb = (blockIdx.x * a.iters + it) * CC::NB + blk;
-        const bool active = gb < a.total_blocks;
-        if (!active) gb = a.total_blocks - 1;  // compute a valid block, skip its store
-        const uint32_t bb = gb & n1mask, q = gb >> a.log_n1;
-        const uint32_t l = q / a.batch, b = q - l * a.batch;
-        uint64_t* g = a.data + (((uint64_t)b * a.L + l) << a.logn) + (uint64_t)bb * M;
-        const uint32_t F = (1u << a.log_n1) + bb;
-        const Tw* tab = a.tab + ((uint64_t)l << a.logn);
-        const Tw* ot = a.ot + (uint64_t)l * (B_ot + ((1u << a.logn) >> a.ot_logb));
-        const PrimeConst pc = a.pc[l];
-        // TWS (Kernel-2 mode): twiddles from the plan's Kernel-2 table, whose
-        // per-round [i][h][g] order makes every warp read contiguous entries.
-        const Tw* tb2 = a.tab2 + ((uint64_t)l << a.logn) + ((uint64_t)bb << LOGM);
-        auto tabf = [&](const TwKey& k) {
-            if constexpr (TWS) {
-                return ldg_tw(tb2 + K2Layout<LOGM, LOGE>::round_off(k.S) + ((((1u << k.i) - 1u + k.h) << k.S) + k.g));
-            } else {
-                return ldg_tw(tab + k.idx + ((F - 1u) << k.j));
-            }
-        };
-        auto otf = [&](uint32_t idx) {
-            // exponent of Psi[idx] is bitrev_logn(idx) = e = q*B + r
-            const uint32_t e = __brev(idx) >> (32 - a.logn);
-            return TwMul<true>{ldg_tw(ot + (e & (B_ot - 1u))), ldg_tw(ot + B_ot + (e >> a.ot_logb))};
-        };
-
-        // Round 0 touches e = o + k s with s = M >> r(0): when s >= 16 a warp's
-        // accesses are whole 128-byte segments, so the forward loads round 0
-        // straight from global and the inverse stores its last round (round 0)
-        // straight to global; the other end goes through SMEM with 16-byte
-        // vectors.
-        constexpr bool DIRECT0 = RoundGeo<LOGM, 0, LOGE>::s >= 16;
-        auto stage_in = [&]() {
-#pragma unroll
-            for (int j = 0; j < E / 2; ++j) {
-                const uint32_t ch = j * TB + tib;
-                ulonglong2 v = *reinterpret_cast<const ulonglong2*>(g + 2 * ch);
-                if constexpr (MUL) {  // fused NTT-domain product (ntt_pointwise_inverse)
-                    const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(a.mul_a + (g - a.data) + 2 * ch);
-                    v.x = mont_mul(u.x, v.x, pc);
-                    v.y = mont_mul(u.y, v.y, pc);
-                }
-                *reinterpret_cast<ulonglong2*>(sb + swz(2 * ch)) = v;
-            }
-            block_sync<TB>(blk);
-        };
-        auto stage_out = [&]() {
-            if (active) {
-#pragma unroll
-                for (int j = 0; j < E / 2; ++j) {
-                    const uint32_t ch = j * TB + tib;
-                    *reinterpret_cast<ulonglong2*>(g + 2 * ch) =
-                        *reinterpret_cast<const ulonglong2*>(sb + swz(2 * ch));
-                }
-            }
-            block_sync<TB>(blk);  // the next iteration reuses this SMEM block
-        };
-
-        uint64_t x[16];
-        auto g_load0 = [&]() {
-            using Geo = RoundGeo<LOGM, 0, LOGE>;
-#pragma unroll
-            for (int qd = 0; qd < Geo::GPT; ++qd)
-#pragma unroll
-                for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = g[Geo::elem(qd * TB + tib, k)];
-        };
-        auto g_store0 = [&]() {
-            using Geo = RoundGeo<LOGM, 0, LOGE>;
-            if (active) {
-#pragma unroll
-                for (int qd = 0; qd < Geo::GPT; ++qd)
-#pragma unroll
-                    for (int k = 0; k < Geo::R; ++k) g[Geo::elem(qd * TB + tib, k)] = x[qd * Geo::R + k];
-            }
-        };
-        // stride-1 rounds hold adjacent pairs (e, e+1): 128-bit SMEM accesses
-        auto s_load = [&](auto ri) {
-            using Geo = RoundGeo<LOGM, decltype(ri)::value, LOGE>;
-#pragma unroll
-            for (int qd = 0; qd < Geo::GPT; ++qd) {
-                if constexpr (Geo::s == 1 && Geo::R >= 2) {
-#pragma unroll
-                    for (int k = 0; k < Geo::R; k += 2) {
-                        const ulonglong2 v =
-                            *reinterpret_cast<const ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k)));
-                        x[qd * Geo::R + k] = v.x;
-                        x[qd * Geo::R + k + 1] = v.y;
-                    }
-                } else {
-#pragma unroll
-                    for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = sb[swz(Geo::elem(qd * TB + tib, k))];
-                }
-            }
-        };
-        auto s_store = [&](auto ri) {
-            using Geo = RoundGeo<LOGM, decltype(ri)::value, LOGE>;
-#pragma unroll
-            for (int qd = 0; qd < Geo::GPT; ++qd) {
-                if constexpr (Geo::s == 1 && Geo::R >= 2) {
-#pragma unroll
-                    for (int k = 0; k < Geo::R; k += 2)
-                        *reinterpret_cast<ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k))) =
-                            make_ulonglong2(x[qd * Geo::R + k], x[qd * Geo::R + k + 1]);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < Geo::R; ++k) sb[swz(Geo::elem(qd * TB + tib, k))] = x[qd * Geo::R + k];
-                }
-            }
-        };
-
-        auto tw_ready = [&]() {};
-        if constexpr (!INV) {
-            if constexpr (!DIRECT0) stage_in();
-            tw_ready();
-            static_for<NR>([&](auto ri) {
-                constexpr int RI = decltype(ri)::value;
-                if constexpr (RI == 0 && DIRECT0) {
-                    g_load0();
-                } else {
-                    s_load(ri);
-                }
-                ct_round<LOGM, LOGE, RI, OT_FROM>(x, tib, F - 1u, tabf, otf, pc);
-                if constexpr (RI == NR - 1) {
-#pragma unroll
-                    for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // [0,8p+2^32) -> [0,p)
-                }
-                s_store(ri);
-                block_sync<TB>(blk);
-            });
-            stage_out();
-        } else {
-            stage_in();
-            tw_ready();
-            static_for<NR>([&](auto rj) {
-                constexpr int RI = NR - 1 - decltype(rj)::value;
-                using RC = std::integral_constant<int, RI>;
-                s_load(RC{});
-                gs_round<LOGM, LOGE, RI, OT_FROM, FUSE0>(x, tib, F - 1u, tabf, otf, pc);
-                if constexpr (FUSE0 && RI == 0) {
-#pragma unroll
-                    for (int k = 0; k < E; ++k) x[k] = norm4(x[k], pc);
-                }
-                if constexpr (RI == 0 && DIRECT0) {
-                    g_store0();
-                } else {
-                    s_store(RC{});
-                    block_sync<TB>(blk);
-                }
-            });
-            if constexpr (!DIRECT0) {
-                stage_out();
-            } else {
-                block_sync<TB>(blk);  // round-0 SMEM reads done before the next stage_in
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------- Kernel-2, pipelined
-// Persistent Kernel-2 / Kernel-2': each group of TB threads ("slot") walks the
-// N2-blocks in a grid-stride loop, prime-major, and prefetches block i+1 into
-// the second half of a double buffer with cp.async (LDGSTS, swizzled
-// destination) while it transforms block i -- the load latency of one block
-// hides behind the arithmetic of the previous one.  Twiddles come through the
-// read-only path (the current prime's table stays L2-resident).
-// The block's twiddles (Kernel-2 layout: one contiguous N2-entry segment per
-// block) are prefetched with the data, so no global load sits on the
-// critical path of a round.  SMEM per slot: 2 x (8 + 16) x N2 bytes.
-template <int LOGM, int LOGE>
-struct PipeCfg {
-    static constexpr int TB = Sched<LOGM, LOGE>::TB;
-    static constexpr int SLOT = (1 << LOGM) * (2 * 8 + 16);  // bytes per slot
-    static constexpr int NB0 = (96 * 1024) / SLOT;
-    static constexpr int NB = NB0 < 1 ? 1 : (NB0 > 4 ? 4 : NB0);  // slots per CTA
-    static constexpr int CT = NB * TB;
-    // double-buffered data, single-buffered twiddles (refilled once the last
-    // round has read them): (2 x 8 + 16) x N2 bytes per slot
-    static constexpr size_t SMEM = (size_t)NB * (1 << LOGM) * (2 * 8 + sizeof(Tw));
-    static constexpr int MINB = LOGE >= 4 ? 3 : 3;
-};
-
-template <int LOGM, int LOGE, bool INV, int OTS, bool MUL = false>
-__global__ void __launch_bounds__(PipeCfg<LOGM, LOGE>::CT, PipeCfg<LOGM, LOGE>::MINB) k_blocks(const KArgs a)
-{
-    using SC = Sched<LOGM, LOGE>;
-    using PC = PipeCfg<LOGM, LOGE>;
-    constexpr int M = SC::M, E = SC::E, TB = SC::TB, NR = SC::NR, NB = PC::NB;
-    constexpr int OT_FROM = OTS ? LOGM - OTS : (1 << 20);
-    static_assert(TB <= 256 && NB >= 1, "block size");
-    extern __shared__ __align__(16) uint64_t sm[];
-
-    const uint32_t tid = threadIdx.x, blk = tid / TB, tib = tid % TB;
-    const uint32_t n1mask = (1u << a.log_n1) - 1u;
-    const uint32_t B_ot = 1u << a.ot_logb;
-    const uint32_t nslots = gridDim.x * NB;
-
-    auto block_ptr = [&](uint32_t gb, uint32_t& l, uint32_t& bb) {
-        bb = gb & n1mask;
-        const uint32_t q = gb >> a.log_n1;  // prime-major: q = l * batch + b
-        l = q / a.batch;
-        const uint32_t b = q - l * a.batch;
-        return a.data + (((uint64_t)b * a.L + l) << a.logn) + (uint64_t)bb * M;
-    };
-    Tw* const tws = reinterpret_cast<Tw*>(sm + 2 * NB * M) + blk * M;
-    auto prefetch_data = [&](uint32_t gb, uint32_t buf) {
-        if (gb < a.total_blocks) {
-            uint32_t l, bb;
-            const uint64_t* g = block_ptr(gb, l, bb);
-            uint64_t* sd = sm + (buf * NB + blk) * M;
-#pragma unroll
-            for (int j = 0; j < E / 2; ++j) {
-                const uint32_t ch = j * TB + tib;
-                cp_async16(sd + swz(2 * ch), g + 2 * ch);
-            }
-        }
-    };
-    auto prefetch_tw = [&](uint32_t gb) {
-        if (gb < a.total_blocks) {
-            const uint32_t bb = gb & n1mask, q = gb >> a.log_n1, l = q / a.batch;
-            const Tw* t2 = a.tab2 + ((uint64_t)l << a.logn) + ((uint64_t)bb << LOGM);
-#pragma unroll
-            for (int j = 0; j < E; ++j) cp_async16(tws + j * TB + tib, t2 + j * TB + tib);
-        }
-    };
-    auto commit = [] { asm volatile("cp.async.commit_group;" ::: "memory"); };
-
-    uint32_t gb = blockIdx.x * NB + blk;
-    prefetch_data(gb, 0);
-    prefetch_tw(gb);
-    commit();
-    for (uint32_t it = 0; gb < a.total_blocks; ++it, gb += nslots) {
-        uint64_t* sb = sm + ((it & 1) * NB + blk) * M;
-        prefetch_data(gb + nslots, (it + 1) & 1);
-        commit();
-        asm volatile("cp.async.wait_group 1;" ::: "memory");  // data(it) and tw(it) landed
-        block_sync<TB>(blk);
-        uint32_t l, bb;
-        uint64_t* g = block_ptr(gb, l, bb);
-        const uint32_t Fm1 = (1u << a.log_n1) + bb - 1u;
-        const Tw* ot = a.ot + (uint64_t)l * (B_ot + ((1u << a.logn) >> a.ot_logb));
-        const PrimeConst pc = a.pc[l];
-        // Kernel-2 table segment (plan-built, per block, per round, [i][h][g]),
-        // prefetched into SMEM: the lanes of a warp read consecutive groups g.
-        auto tabf = [&](const TwKey& k) {
-            return tws[K2Layout<LOGM, LOGE>::round_off(k.S) + ((((1u << k.i) - 1u + k.h) << k.S) + k.g)];
-        };
-        auto otf = [&](uint32_t idx) {
-            const uint32_t e = __brev(idx) >> (32 - a.logn);  // exponent of Psi[idx]
-            return TwMul<true>{ldg_tw(ot + (e & (B_ot - 1u))), ldg_tw(ot + B_ot + (e >> a.ot_logb))};
-        };
-
-        uint64_t x[16];
-        auto s_load = [&](auto ri) {
-            using Geo = RoundGeo<LOGM, decltype(ri)::value, LOGE>;
-#pragma unroll
-            for (int qd = 0; qd < Geo::GPT; ++qd) {
-                if constexpr (Geo::s == 1 && Geo::R >= 2) {
-#pragma unroll
-                    for (int k = 0; k < Geo::R; k += 2) {
-                        const ulonglong2 v =
-                            *reinterpret_cast<const ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k)));
-                        x[qd * Geo::R + k] = v.x;
-                        x[qd * Geo::R + k + 1] = v.y;
-                    }
-                } else {
-#pragma unroll
-                    for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = sb[swz(Geo::elem(qd * TB + tib, k))];
-                }
-            }
-        };
-        auto s_store = [&](auto ri) {
-            using Geo = RoundGeo<LOGM, decltype(ri)::value, LOGE>;
-#pragma unroll
-            for (int qd = 0; qd < Geo::GPT; ++qd) {
-                if constexpr (Geo::s == 1 && Geo::R >= 2) {
-#pragma unroll
-                    for (int k = 0; k < Geo::R; k += 2)
-                        *reinterpret_cast<ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k))) =
-                            make_ulonglong2(x[qd * Geo::R + k], x[qd * Geo::R + k + 1]);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < Geo::R; ++k) sb[swz(Geo::elem(qd * TB + tib, k))] = x[qd * Geo::R + k];
-                }
-            }
-        };
-        auto stage_out = [&]() {
-#pragma unroll
-            for (int j = 0; j < E / 2; ++j) {
-                const uint32_t ch = j * TB + tib;
-                *reinterpret_cast<ulonglong2*>(g + 2 * ch) = *reinterpret_cast<const ulonglong2*>(sb + swz(2 * ch));
-            }
-        };
-        constexpr bool DIRECT0 = RoundGeo<LOGM, 0, LOGE>::s >= 16;
-
-        if constexpr (!INV) {
-            static_for<NR>([&](auto ri) {
-                constexpr int RI = decltype(ri)::value;
-                s_load(ri);
-                ct_round<LOGM, LOGE, RI, OT_FROM>(x, tib, Fm1, tabf, otf, pc);
-                if constexpr (RI == NR - 1) {
-#pragma unroll
-                    for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // [0,8p+2^32) -> [0,p)
-                }
-                s_store(ri);
-                block_sync<TB>(blk);
-            });
-            prefetch_tw(gb + nslots);  // the sync above ended every twiddle read
-            commit();
-            stage_out();
-        } else {
-            static_for<NR>([&](auto rj) {
-                constexpr int RI = NR - 1 - decltype(rj)::value;
-                using RC = std::integral_constant<int, RI>;
-                s_load(RC{});
-                if constexpr (MUL && RI == NR - 1) {  // fused NTT-domain product (ntt_pointwise_inverse)
-                    using Geo = RoundGeo<LOGM, RI, LOGE>;
-                    const uint64_t* ga = a.mul_a + (g - a.data);
-#pragma unroll
-                    for (int qd = 0; qd < Geo::GPT; ++qd)
-#pragma unroll
-                        for (int k = 0; k < Geo::R; ++k)
-                            x[qd * Geo::R + k] = mont_mul(__ldg(ga + Geo::elem(qd * TB + tib, k)), x[qd * Geo::R + k], pc);
-                }
-                gs_round<LOGM, LOGE, RI, OT_FROM, false>(x, tib, Fm1, tabf, otf, pc);
-                if constexpr (RI == 0 && DIRECT0) {
-                    using Geo = RoundGeo<LOGM, 0, LOGE>;
-#pragma unroll
-                    for (int qd = 0; qd < Geo::GPT; ++qd)
-#pragma unroll
-                        for (int k = 0; k < Geo::R; ++k) g[Geo::elem(qd * TB + tib, k)] = x[qd * Geo::R + k];
-                } else {
-                    s_store(RC{});
-                    block_sync<TB>(blk);
-                }
-            });
-            if constexpr (!DIRECT0) stage_out();
-        }
-        block_sync<TB>(blk);  // all reads of this buffer done before it is refilled
-        if constexpr (INV) {
-            prefetch_tw(gb + nslots);
-            commit();
-        }
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-}
 
 // ---------------------------------------------------------------- element-wise product
 // b <- a (.) b 2^-64 for every word (unfused path of ntt_pointwise_inverse;
@@ -685,203 +29,21 @@ cudaError_t launch_pointwise(const KArgs& a, cudaStream_t st)
     return cudaPeekAtLastError();
 }
 
-// ---------------------------------------------------------------- dispatch
-#ifndef NTT_KERNELS_ONLY  // tools/sass_probe.sh compiles the kernels alone
-namespace {
-
-// SM count of the current device, cached per device (persistent-grid sizing)
-int sm_count()
+cudaError_t launch_single(bool inverse, const KArgs& a, int ots, uint32_t iters, cudaStream_t st, bool proth)
 {
-    static std::atomic<int> cache[64];
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int v = cache[dev & 63].load(std::memory_order_relaxed);
-    if (v == 0) {
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        cache[dev & 63].store(v, std::memory_order_relaxed);
-    }
-    return v;
+    return proth ? launch_single_p(inverse, a, ots, iters, st)
+                 : launch_single_t<PrimeConst>(inverse, a, ots, iters, st);
 }
 
-// true if this device already had the attribute set; marks it otherwise
-bool set_once(std::atomic<uint64_t>& mask)
+cudaError_t launch_k2(bool inverse, int loge, const KArgs& a, int ots, uint32_t iters, cudaStream_t st, bool proth)
 {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const uint64_t bit = 1ull << (dev & 63);
-    return mask.fetch_or(bit) & bit;
+    return proth ? launch_k2_p(inverse, loge, a, ots, iters, st)
+                 : launch_k2_t<PrimeConst>(inverse, loge, a, ots, iters, st);
 }
 
-template <int LOGN1, int LOGN, int LOGE, bool INV>
-cudaError_t launch_cols_t(const KArgs& a, uint32_t rows, cudaStream_t st)
+cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st, bool proth)
 {
-    using CC = ColsCfg<LOGN1, LOGE>;
-    auto fn = k_cols<LOGN1, LOGN, LOGE, INV>;
-    static std::atomic<uint64_t> attr_set{0};  // one bit per device
-    if (!set_once(attr_set)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
-    const uint64_t grid = (uint64_t)rows << a.log_tiles;
-    fn<<<(unsigned)grid, CC::CT, CC::SMEM, st>>>(a);
-    return cudaPeekAtLastError();
+    return proth ? launch_k1_p(inverse, loge, a, rows, st) : launch_k1_t<PrimeConst>(inverse, loge, a, rows, st);
 }
 
-template <int LOGM, int LOGE, bool INV, bool FUSE0, int OTS, bool TWS, bool MUL = false>
-cudaError_t launch_contig_t(KArgs a, uint32_t iters, cudaStream_t st)
-{
-    using CC = ContigCfg<LOGM, LOGE, TWS>;
-    auto fn = k_contig<LOGM, LOGE, INV, FUSE0, OTS, TWS, MUL>;
-    static std::atomic<uint64_t> attr_set{0};  // one bit per device
-    if (!set_once(attr_set)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
-    a.iters = iters;
-    const uint64_t per_cta = (uint64_t)CC::NB * iters;
-    const uint64_t grid = (a.total_blocks + per_cta - 1) / per_cta;
-    fn<<<(unsigned)grid, CC::CT, CC::SMEM, st>>>(a);
-    return cudaPeekAtLastError();
-}
-
-template <int LOGM, int LOGE, bool INV, int OTS, bool MUL = false>
-cudaError_t launch_blocks_t(KArgs a, cudaStream_t st)
-{
-    using PC = PipeCfg<LOGM, LOGE>;
-    auto fn = k_blocks<LOGM, LOGE, INV, OTS, MUL>;
-    static std::atomic<uint64_t> attr_set{0};  // one bit per device
-    static int ctas_per_sm = 0;
-    if (!set_once(attr_set)) {
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC::SMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, fn, PC::CT, PC::SMEM);
-    }
-    const int sms = sm_count();
-    const uint64_t want = ((uint64_t)a.total_blocks + PC::NB - 1) / PC::NB;
-    const uint64_t grid = std::min<uint64_t>(want, (uint64_t)sms * std::max(1, ctas_per_sm));
-    fn<<<(unsigned)grid, PC::CT, PC::SMEM, st>>>(a);
-    return cudaPeekAtLastError();
-}
-
-template <int LOGM, int LOGE, bool INV>
-cudaError_t launch_blocks_ot(const KArgs& a, int ots, cudaStream_t st)
-{
-    if (a.mul_a) {  // fused product only in the radix-16 inverse without OT; else the caller unfuses
-        if constexpr (INV && LOGE == 4) {
-            if (ots == 0) return launch_blocks_t<LOGM, LOGE, INV, 0, true>(a, st);
-        }
-        return cudaErrorNotSupported;
-    }
-    switch (ots) {
-        case 0: return launch_blocks_t<LOGM, LOGE, INV, 0>(a, st);
-        case 1: return launch_blocks_t<LOGM, LOGE, INV, 1>(a, st);
-        default: return launch_blocks_t<LOGM, LOGE, INV, 2>(a, st);
-    }
-}
-
-template <int LOGE, bool INV, int... Ls>
-cudaError_t blocks_switch(int logm, const KArgs& a, int ots, cudaStream_t st, std::integer_sequence<int, Ls...>)
-{
-    cudaError_t err = cudaErrorInvalidValue;
-    ((logm == Ls ? (err = launch_blocks_ot<Ls, LOGE, INV>(a, ots, st), 0) : 0), ...);
-    return err;
-}
-
-template <int LOGM, int LOGE, bool INV, bool FUSE0, bool TWS>
-cudaError_t launch_contig_ot(const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
-{
-    if (a.mul_a) {  // fused product only in the radix-16 inverse without OT; else the caller unfuses
-        if constexpr (INV && LOGE == 4) {
-            if (ots == 0) return launch_contig_t<LOGM, LOGE, INV, FUSE0, 0, TWS, true>(a, iters, st);
-        }
-        return cudaErrorNotSupported;
-    }
-    switch (ots) {
-        case 0: return launch_contig_t<LOGM, LOGE, INV, FUSE0, 0, TWS>(a, iters, st);
-        case 1: return launch_contig_t<LOGM, LOGE, INV, FUSE0, 1, TWS>(a, iters, st);
-        default: return launch_contig_t<LOGM, LOGE, INV, FUSE0, (LOGM >= 2 ? 2 : LOGM), TWS>(a, iters, st);
-    }
-}
-
-template <int LOGE, bool INV, bool FUSE0, bool TWS, int... Ls>
-cudaError_t contig_switch(int logm, const KArgs& a, int ots, uint32_t iters, cudaStream_t st,
-                          std::integer_sequence<int, Ls...>)
-{
-    cudaError_t err = cudaErrorInvalidValue;
-    ((logm == Ls ? (err = launch_contig_ot<Ls, LOGE, INV, FUSE0, TWS>(a, ots, iters, st), 0) : 0), ...);
-    return err;
-}
-
-template <int LOGN1, int LOGN, int LOGE, bool INV>
-cudaError_t launch_cols_pipe_t(const KArgs& a, uint32_t rows, cudaStream_t st)
-{
-    using CC = ColsPipeCfg<LOGN1, LOGE>;
-    auto fn = k_cols_pipe<LOGN1, LOGN, LOGE, INV>;
-    static std::atomic<uint64_t> attr_set{0};  // one bit per device
-    static int ctas_per_sm = 0;
-    if (!set_once(attr_set)) {
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, fn, CC::CT, CC::SMEM);
-    }
-    const int sms = sm_count();
-    const uint64_t want = (uint64_t)rows << a.log_tiles;
-    const uint64_t grid = std::min<uint64_t>(want, (uint64_t)sms * std::max(1, ctas_per_sm));
-    fn<<<(unsigned)grid, CC::CT, CC::SMEM, st>>>(a);
-    return cudaPeekAtLastError();
-}
-
-template <bool INV, int... Ks>
-cudaError_t cols_pipe_switch(int key, const KArgs& a, uint32_t rows, cudaStream_t st, std::integer_sequence<int, Ks...>)
-{
-    cudaError_t err = cudaErrorInvalidValue;
-    ((key == Ks ? (err = launch_cols_pipe_t<(Ks & 15), (Ks >> 4), 4, INV>(a, rows, st), 0) : 0), ...);
-    return err;
-}
-
-// Ks encodes (logn << 4) | log_n1
-template <int LOGE, bool INV, int... Ks>
-cudaError_t cols_switch(int key, const KArgs& a, uint32_t rows, cudaStream_t st, std::integer_sequence<int, Ks...>)
-{
-    cudaError_t err = cudaErrorInvalidValue;
-    ((key == Ks ? (err = launch_cols_t<(Ks & 15), (Ks >> 4), LOGE, INV>(a, rows, st), 0) : 0), ...);
-    return err;
-}
-
-}  // namespace
-
-// Supported sizes: single kernel LOGM 1..13; Kernel-2 LOGM 6..11; Kernel-1 (logn, log_n1) pairs below.
-using SingleSizes = std::integer_sequence<int, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13>;
-using K2Sizes = std::integer_sequence<int, 6, 7, 8, 9, 10, 11>;
-#define K1P(n, n1) (((n) << 4) | (n1))
-using K1Pairs = std::integer_sequence<int, K1P(14, 6), K1P(14, 7), K1P(14, 8), K1P(15, 6), K1P(15, 7), K1P(15, 8),
-                                      K1P(15, 9), K1P(16, 6), K1P(16, 7), K1P(16, 8), K1P(16, 9), K1P(16, 10),
-                                      K1P(17, 6), K1P(17, 7), K1P(17, 8), K1P(17, 9), K1P(17, 10)>;
-#undef K1P
-
-cudaError_t launch_single(bool inverse, const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
-{
-    return inverse ? contig_switch<4, true, true, false>((int)a.logn, a, ots, iters, st, SingleSizes{})
-                   : contig_switch<4, false, false, false>((int)a.logn, a, ots, iters, st, SingleSizes{});
-}
-
-cudaError_t launch_k2(bool inverse, int loge, const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
-{
-    const int logm = (int)(a.logn - a.log_n1);
-    if (loge == 5)  // pipelined persistent Kernel-2 (radix 16)
-        return inverse ? blocks_switch<4, true>(logm, a, ots, st, K2Sizes{})
-                       : blocks_switch<4, false>(logm, a, ots, st, K2Sizes{});
-    if (loge == 6)  // pipelined persistent Kernel-2 (radix 8)
-        return inverse ? blocks_switch<3, true>(logm, a, ots, st, K2Sizes{})
-                       : blocks_switch<3, false>(logm, a, ots, st, K2Sizes{});
-    if (loge == 3)
-        return inverse ? contig_switch<3, true, false, true>(logm, a, ots, iters, st, K2Sizes{})
-                       : contig_switch<3, false, false, true>(logm, a, ots, iters, st, K2Sizes{});
-    return inverse ? contig_switch<4, true, false, true>(logm, a, ots, iters, st, K2Sizes{})
-                   : contig_switch<4, false, false, true>(logm, a, ots, iters, st, K2Sizes{});
-}
-
-cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st)
-{
-    const int key = (int)((a.logn << 4) | a.log_n1);
-    if (loge == 5 && a.log_n1 <= 9)  // pipelined persistent Kernel-1 (radix 16); SMEM caps N1 at 2^9
-        return inverse ? cols_pipe_switch<true>(key, a, rows, st, K1Pairs{})
-                       : cols_pipe_switch<false>(key, a, rows, st, K1Pairs{});
-    return inverse ? cols_switch<4, true>(key, a, rows, st, K1Pairs{})
-                   : cols_switch<4, false>(key, a, rows, st, K1Pairs{});
-}
-
-#endif  // NTT_KERNELS_ONLY
 }  // namespace ntt

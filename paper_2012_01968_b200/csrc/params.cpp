@@ -61,6 +61,11 @@ bool ntt_primes(uint64_t N, unsigned count, std::vector<uint64_t>& out)
     return true;
 }
 
+bool proth_primes(unsigned count, std::vector<uint64_t>& out)
+{
+    return ntt_primes(1ull << 31, count, out);  // step 2^32: p = k 2^32 + 1
+}
+
 bool ntt_primes32(uint64_t N, unsigned count, std::vector<uint32_t>& out)
 {
     out.clear();

@@ -21,6 +21,9 @@ Twiddle shoup_pair(uint64_t w, uint64_t p);
 // NTT primes p = 1 mod 2N in [2^59, 2^60), descending from 2^60 - 2N + 1.
 // Returns false if the range is exhausted before `count` primes.
 bool ntt_primes(uint64_t N, unsigned count, std::vector<uint64_t>& out);
+// Proth-form NTT primes p = k 2^32 + 1 in [2^59, 2^60), descending from
+// 2^60 - 2^32 + 1 (ntt_find_primes_ex, NTT_PRIMES_PROTH32).
+bool proth_primes(unsigned count, std::vector<uint64_t>& out);
 
 // 32-bit word path (NEXT-4): primes p = 1 mod 2N in [2^29, 2^30), descending
 // from 2^30 - 2N + 1; and the 32-bit Shoup pair wb = floor(w 2^32 / p).

@@ -149,3 +149,30 @@ def test_product_package_does_not_touch_oracle():
                 assert not pat.search(src), f
     out = os.popen(f"nm -D {_native.LIB_PATH}").read()
     assert "oracle_" not in out
+
+
+@pytest.mark.parametrize("logn,count", [(1, 2), (12, 4), (17, 60), (17, 64)])
+def test_host_proth_primes_match_oracle(logn, count):
+    """NTT_PRIMES_PROTH32: p = k 2^32 + 1 in [2^59, 2^60) (P:423 range; = 1 mod
+    2N for every N <= 2^17, P:274 / R1), descending -- the oracle's own scan
+    with step 2^32 finds the same list."""
+    N = 1 << logn
+    got = find_primes(N, count, "proth")
+    assert got == oracle.find_primes(1 << 31, count)
+    assert all(p % (1 << 32) == 1 and (1 << 59) <= p < (1 << 60) for p in got)
+    assert got == sorted(got, reverse=True) and len(set(got)) == count
+    # no prime of the family was skipped between the first and the last
+    k_hi, k_lo = got[0] >> 32, got[-1] >> 32
+    found = {p >> 32 for p in got}
+    for k in range(k_lo, k_hi + 1):
+        if k not in found:
+            assert not oracle.is_prime((k << 32) + 1)
+    assert (((1 << 28) - 1) << 32) + 1 >= got[0]
+
+
+def test_proth_primes_errors():
+    lib = _native.lib()
+    out = (ctypes.c_uint64 * 2)()
+    assert lib.ntt_find_primes_ex(1 << 12, 2, 7, out) == -3  # unknown form
+    assert lib.ntt_find_primes_ex(3, 2, 1, out) == -1
+    assert lib.ntt_find_primes_ex(1 << 12, 0, 1, out) == -3

@@ -295,3 +295,43 @@ def test_kernel2_variants(variant, logn, log_n1, monkeypatch):
     monkeypatch.setenv("NTT_LOGE", variant)
     check_roundtrip(1 << logn, 3, 2, log_n1=log_n1)
     check_roundtrip(1 << logn, 2, 1, log_n1=log_n1, ot=True)
+
+
+@pytest.mark.parametrize("logn", [14, 15, 16, 17])
+@pytest.mark.parametrize("L,batch", [(1, 1), (3, 2), (5, 3)])
+def test_fused_cluster_kernel(logn, L, batch):
+    """NEXT-1: the single-pass cluster kernel (N/2^13 CTAs per row, DSMEM
+    exchange) equals the oracle for every cluster size 2..16."""
+    plan = Plan(1 << logn, chain(1 << logn, L)[0], fused=True)
+    info = plan.info()
+    assert info["passes"] == 1 and info["cluster"] == 1 << (logn - 13)
+    plan.close()
+    check_roundtrip(1 << logn, L, batch, config_id=31, fused=True)
+
+
+@pytest.mark.parametrize("logn", [14, 17])
+def test_fused_vs_two_kernel_identical(logn):
+    """The fused and the two-kernel paths give the same words (both equal the
+    oracle, which is exact)."""
+    N = 1 << logn
+    primes, psis = chain(N, 2)
+    x = synth.rns_rows(primes, 2, N, config_id=33)
+    outs = []
+    for fused in (True, False):
+        plan = Plan(N, primes, fused=fused)
+        assert plan.info()["passes"] == (1 if fused else 2)
+        d = to_dev(x)
+        plan.forward(d)
+        outs.append(to_host(d))
+        plan.close()
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], oracle.ntt_batch(x.copy(), primes, psis, +1))
+
+
+def test_fused_option_errors():
+    N = 1 << 13
+    with pytest.raises(NttError):
+        Plan(N, chain(N, 1)[0], fused=True)  # one CTA holds the row: no cluster kernel
+    N = 1 << 16
+    with pytest.raises(NttError):
+        Plan(N, chain(N, 1)[0], fused=True, ot=True)

@@ -21,10 +21,11 @@ ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--ot", action="store_true")
 ap.add_argument("--log-n1", type=int, default=0)
+ap.add_argument("--primes", default="2n", choices=["2n", "proth"])
 a = ap.parse_args()
 logn, L, B, _ = CONFIGS[a.config]
 N = 1 << logn
-primes = find_primes(N, L)
+primes = find_primes(N, L, a.primes)
 x = synth.rns_rows(primes, B, N, config_id=synth.CONFIG_IDS[a.config])
 d = torch.from_numpy(x.view(np.int64)).cuda()
 plan = Plan(N, primes, ot=a.ot, log_n1=a.log_n1)

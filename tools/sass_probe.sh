@@ -1,17 +1,17 @@
 #!/bin/bash
 # Static SASS opcode counts of the C4 kernels (no GPU), for quick experiments
-# on the arithmetic formulation:  tools/sass_probe.sh [extra nvcc flags]
+# on the arithmetic formulation:  [PCT=PrimeConstP] tools/sass_probe.sh [extra nvcc flags]
 set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 T=$(mktemp -d)
+PCT=${PCT:-PrimeConst}
 cat > $T/p.cu <<EOT
-#define NTT_KERNELS_ONLY
-#include "$ROOT/paper_2012_01968_b200/csrc/ntt_kernels.cu"
+#include "$ROOT/paper_2012_01968_b200/csrc/ntt_kernels.cuh"
 namespace ntt {
-template __global__ void k_cols<8, 17, 4, false>(const KArgs);
-template __global__ void k_cols<8, 17, 4, true>(const KArgs);
-template __global__ void k_blocks<9, 4, false, 0, false>(const KArgs);
-template __global__ void k_blocks<9, 4, true, 0, false>(const KArgs);
+template __global__ void k_cols<8, 17, 4, false, $PCT>(const KArgs);
+template __global__ void k_cols<8, 17, 4, true, $PCT>(const KArgs);
+template __global__ void k_blocks<9, 4, false, 0, false, $PCT>(const KArgs);
+template __global__ void k_blocks<9, 4, true, 0, false, $PCT>(const KArgs);
 }
 EOT
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I $ROOT/include "$@" -cubin -o $T/p.cubin $T/p.cu -Xptxas -v 2>&1 | grep -E "registers|spill" | grep -v "0 bytes spill" || true
