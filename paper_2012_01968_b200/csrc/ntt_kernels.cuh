@@ -478,6 +478,161 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
     }
 }
 
+// ---------------------------------------------------------------- Kernel-2, shared twiddles
+// Kernel-2 / Kernel-2' with one CTA per (prime l, block position bb, group of
+// NB ciphertexts): the NB blocks of a CTA use the same twiddles (Psi depends on
+// the prime and the block position only), so the block's Kernel-2 table segment
+// (N2 entries, plan-built K2Layout) is staged in SMEM once and read by all NB
+// block groups; each block is transformed by TB = N2/16 threads (one warp for
+// N2 = 2^9) that synchronise among themselves only.  256 threads, 64 registers:
+// 4 CTAs = 32 warps per SM, like Kernel-1, so the multiply pipe is fed by
+// occupancy rather than by a software pipeline.
+template <int LOGM>
+struct SharedCfg {
+    static constexpr int TB = Sched<LOGM, 4>::TB;
+    static constexpr int CT = 256;
+    static constexpr int NB = CT / TB;  // blocks (ciphertexts) per CTA
+    static constexpr size_t SMEM = (size_t)NB * (8u << LOGM) + (sizeof(Tw) << LOGM);
+    static constexpr int MINB = 4;
+};
+
+template <int LOGM, bool INV, int OTS, bool MUL = false, class PCT = PrimeConst>
+__global__ void __launch_bounds__(SharedCfg<LOGM>::CT, SharedCfg<LOGM>::MINB) k_shared(const KArgs a)
+{
+    using SC = Sched<LOGM, 4>;
+    using CC = SharedCfg<LOGM>;
+    constexpr int M = SC::M, E = SC::E, TB = SC::TB, NR = SC::NR, NB = CC::NB, CT = CC::CT;
+    constexpr int OT_FROM = OTS ? LOGM - OTS : (1 << 20);
+    extern __shared__ __align__(16) uint64_t sm[];
+    Tw* const tws = reinterpret_cast<Tw*>(sm + NB * M);
+
+    const uint32_t tid = threadIdx.x, blk = tid / TB, tib = tid % TB;
+    // CTA -> (l, bb, ciphertext group), prime-major then block position
+    const uint32_t groups = (a.batch + NB - 1) / NB;
+    const uint32_t cg = blockIdx.x % groups, rest = blockIdx.x / groups;
+    const uint32_t bb = rest & ((1u << a.log_n1) - 1u), l = rest >> a.log_n1;
+    const uint32_t b = cg * NB + blk;
+    const bool active = b < a.batch;
+    uint64_t* g = a.data + (((uint64_t)(active ? b : 0) * a.L + l) << a.logn) + ((uint64_t)bb << LOGM);
+    const uint32_t Fm1 = (1u << a.log_n1) + bb - 1u;
+    const uint32_t B_ot = 1u << a.ot_logb;
+    const Tw* ot = a.ot + (uint64_t)l * (B_ot + ((1u << a.logn) >> a.ot_logb));
+    const PCT pc = load_pc<PCT>(a.pc, l);
+
+    {  // the block position's twiddle segment, once per CTA
+        const Tw* t2 = a.tab2 + ((uint64_t)l << a.logn) + ((uint64_t)bb << LOGM);
+        for (uint32_t i = tid; i < (uint32_t)M; i += CT) cp_async16(tws + i, t2 + i);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    uint64_t* sb = sm + blk * M;
+    auto tabf = [&](const TwKey& k) {
+        return tws[K2Layout<LOGM, 4>::round_off(k.S) + ((((1u << k.i) - 1u + k.h) << k.S) + k.g)];
+    };
+    auto otf = [&](uint32_t idx) {
+        const uint32_t e = __brev(idx) >> (32 - a.logn);  // exponent of Psi[idx]
+        return TwMul<true>{ldg_tw(ot + (e & (B_ot - 1u))), ldg_tw(ot + B_ot + (e >> a.ot_logb))};
+    };
+
+    uint64_t x[16];
+    auto s_load = [&](auto ri) {
+        using Geo = RoundGeo<LOGM, decltype(ri)::value, 4>;
+#pragma unroll
+        for (int qd = 0; qd < Geo::GPT; ++qd) {
+            if constexpr (Geo::s == 1 && Geo::R >= 2) {
+#pragma unroll
+                for (int k = 0; k < Geo::R; k += 2) {
+                    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k)));
+                    x[qd * Geo::R + k] = v.x;
+                    x[qd * Geo::R + k + 1] = v.y;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = sb[swz(Geo::elem(qd * TB + tib, k))];
+            }
+        }
+    };
+    auto s_store = [&](auto ri) {
+        using Geo = RoundGeo<LOGM, decltype(ri)::value, 4>;
+#pragma unroll
+        for (int qd = 0; qd < Geo::GPT; ++qd) {
+            if constexpr (Geo::s == 1 && Geo::R >= 2) {
+#pragma unroll
+                for (int k = 0; k < Geo::R; k += 2)
+                    *reinterpret_cast<ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k))) =
+                        make_ulonglong2(x[qd * Geo::R + k], x[qd * Geo::R + k + 1]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < Geo::R; ++k) sb[swz(Geo::elem(qd * TB + tib, k))] = x[qd * Geo::R + k];
+            }
+        }
+    };
+    constexpr bool DIRECT0 = RoundGeo<LOGM, 0, 4>::s >= 16;
+    static_assert(DIRECT0, "round 0 is read / written straight from global");
+    auto twiddles_ready = [&]() {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+    };
+
+    if constexpr (!INV) {
+        {  // round 0 straight from global: whole 128-byte segments per warp
+            using Geo = RoundGeo<LOGM, 0, 4>;
+#pragma unroll
+            for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+                for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = g[Geo::elem(qd * TB + tib, k)];
+        }
+        twiddles_ready();
+        static_for<NR>([&](auto ri) {
+            constexpr int RI = decltype(ri)::value;
+            if constexpr (RI > 0) s_load(ri);
+            ct_round<LOGM, 4, RI, OT_FROM>(x, tib, Fm1, tabf, otf, pc);
+            if constexpr (RI == NR - 1) {
+#pragma unroll
+                for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // [0,8p+2^32) -> [0,p)
+            }
+            s_store(ri);
+            block_sync<TB>(blk);
+        });
+        if (active) {
+#pragma unroll
+            for (int j = 0; j < E / 2; ++j) {
+                const uint32_t ch = j * TB + tib;
+                *reinterpret_cast<ulonglong2*>(g + 2 * ch) = *reinterpret_cast<const ulonglong2*>(sb + swz(2 * ch));
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < E / 2; ++j) {
+            const uint32_t ch = j * TB + tib;
+            ulonglong2 v = *reinterpret_cast<const ulonglong2*>(g + 2 * ch);
+            if constexpr (MUL) {  // fused NTT-domain product (ntt_pointwise_inverse)
+                const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(a.mul_a + (g - a.data) + 2 * ch);
+                v.x = mont_mul(u.x, v.x, pc);
+                v.y = mont_mul(u.y, v.y, pc);
+            }
+            *reinterpret_cast<ulonglong2*>(sb + swz(2 * ch)) = v;
+        }
+        twiddles_ready();
+        static_for<NR>([&](auto rj) {
+            constexpr int RI = NR - 1 - decltype(rj)::value;
+            using RC = std::integral_constant<int, RI>;
+            s_load(RC{});
+            gs_round<LOGM, 4, RI, OT_FROM, false>(x, tib, Fm1, tabf, otf, pc);
+            if constexpr (RI > 0) {
+                s_store(RC{});
+                block_sync<TB>(blk);
+            }
+        });
+        if (active) {  // round 0 straight to global
+            using Geo = RoundGeo<LOGM, 0, 4>;
+#pragma unroll
+            for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+                for (int k = 0; k < Geo::R; ++k) g[Geo::elem(qd * TB + tib, k)] = x[qd * Geo::R + k];
+        }
+    }
+}
+
 // ---------------------------------------------------------------- Kernel-2, pipelined
 // Persistent Kernel-2 / Kernel-2': each group of TB threads ("slot") walks the
 // N2-blocks in a grid-stride loop, prime-major, and prefetches block i+1 into
@@ -736,6 +891,46 @@ cudaError_t launch_blocks_t(KArgs a, cudaStream_t st)
     return cudaPeekAtLastError();
 }
 
+template <int LOGM, bool INV, int OTS, bool MUL, class PCT>
+cudaError_t launch_shared_t(const KArgs& a, cudaStream_t st)
+{
+    using CC = SharedCfg<LOGM>;
+    auto fn = k_shared<LOGM, INV, OTS, MUL, PCT>;
+    static std::atomic<uint64_t> attr_set{0};  // one bit per device
+    if (!set_once(attr_set)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
+    const uint64_t grid = ((uint64_t)a.L << a.log_n1) * ((a.batch + CC::NB - 1) / CC::NB);
+    fn<<<(unsigned)grid, CC::CT, CC::SMEM, st>>>(a);
+    return cudaPeekAtLastError();
+}
+
+template <int LOGM, bool INV, class PCT>
+cudaError_t launch_shared_ot(const KArgs& a, int ots, cudaStream_t st)
+{
+    if constexpr (RoundGeo<LOGM, 0, 4>::s < 16) {
+        return cudaErrorNotSupported;
+    } else {
+        if (a.mul_a) {
+            if constexpr (INV) {
+                if (ots == 0) return launch_shared_t<LOGM, INV, 0, true, PCT>(a, st);
+            }
+            return cudaErrorNotSupported;
+        }
+        switch (ots) {
+            case 0: return launch_shared_t<LOGM, INV, 0, false, PCT>(a, st);
+            case 1: return launch_shared_t<LOGM, INV, 1, false, PCT>(a, st);
+            default: return launch_shared_t<LOGM, INV, 2, false, PCT>(a, st);
+        }
+    }
+}
+
+template <bool INV, class PCT, int... Ls>
+cudaError_t shared_switch(int logm, const KArgs& a, int ots, cudaStream_t st, std::integer_sequence<int, Ls...>)
+{
+    cudaError_t err = cudaErrorInvalidValue;
+    ((logm == Ls ? (err = launch_shared_ot<Ls, INV, PCT>(a, ots, st), 0) : 0), ...);
+    return err;
+}
+
 template <int LOGM, int LOGE, bool INV, class PCT>
 cudaError_t launch_blocks_ot(const KArgs& a, int ots, cudaStream_t st)
 {
@@ -849,6 +1044,9 @@ cudaError_t launch_k2_t(bool inverse, int loge, const KArgs& a, int ots, uint32_
 {
     using namespace detail;
     const int logm = (int)(a.logn - a.log_n1);
+    if (loge == 7)  // shared-twiddle Kernel-2 (radix 16, one CTA per block position x 256/TB ciphertexts)
+        return inverse ? shared_switch<true, PCT>(logm, a, ots, st, K2Sizes{})
+                       : shared_switch<false, PCT>(logm, a, ots, st, K2Sizes{});
     if (loge == 5)  // pipelined persistent Kernel-2 (radix 16)
         return inverse ? blocks_switch<4, true, PCT>(logm, a, ots, st, K2Sizes{})
                        : blocks_switch<4, false, PCT>(logm, a, ots, st, K2Sizes{});

@@ -10,5 +10,5 @@ timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 timeout 600 python bench.py --primes $PRIMES > $O/bench.json 2> $O/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv python tools/profile_step.py --warmup 1 --primes $PRIMES > $O/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_cols|k_blocks" -s 4 -c 4 -o $O/prof python tools/profile_step.py --warmup 1 --primes $PRIMES > $O/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_cols|k_blocks|k_shared|k_fused" -s 4 -c 4 -o $O/prof python tools/profile_step.py --warmup 1 --primes $PRIMES > $O/ncu_full.log 2>&1
 echo done
