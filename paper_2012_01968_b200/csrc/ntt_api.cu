@@ -374,7 +374,9 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
                 for (int it = 0; it < 6; ++it) inv *= 2 - q * inv;
                 c.pinv = 0 - inv;
                 c.m1 = 0u - (uint32_t)(q >> 32);
-                c.proth = (uint32_t)q == 1u;
+                c.p8 = 8 * q;
+                c.p8_hi = (uint32_t)((8 * q) >> 32);
+                c.zero = 0;
                 nttp::Twiddle t1 = nttp::shoup_pair(ninv, q), t2 = nttp::shoup_pair(ninv_psi, q);
                 c.ninv = Tw{t1.w, t1.wb};
                 c.ninv_psi = Tw{t2.w, t2.wb};

@@ -27,7 +27,9 @@ struct __align__(16) PrimeConst {
     Tw ninv_psi;         // N^-1 * Psi^-1[1], the fused last GS stage (R15)
     uint64_t pinv;       // -p^-1 mod 2^64 (Montgomery, NTT-domain products)
     uint32_t m1;         // 2^32 - (p >> 32): the Proth form below
-    uint32_t proth;      // 1 if p = 1 mod 2^32 (set by the plan)
+    uint32_t p8_hi;      // high word of 8p
+    uint64_t p8;         // 8p: Proth primes reduce by 8p on every other stage (ct_bf)
+    uint64_t zero;       // 0, opaque to the compiler: a third operand that keeps 64-bit adds on IADD3
 };
 
 // The same constants, as a type that selects the Proth-prime arithmetic: for
@@ -128,45 +130,83 @@ __device__ __forceinline__ uint64_t shoup_lazy(uint64_t b, uint64_t w, uint64_t 
 // Shoup's modmul for a Proth prime p = p1 2^32 + 1: the same truncated
 // quotient q' (so the same [0, 4p) output bound), and
 //   r = b w - q' p = lo64(b w) - q' - (q0' p1 << 32)  (mod 2^64),
-// formed as one IMAD.WIDE b0 w0 with the addend -q' plus three IMADs into the
-// high word (m1 = -p1 mod 2^32): 2 IMAD.WIDE, 2 IMAD.HI and 3 IMAD in all.
-__device__ __forceinline__ uint64_t shoup_lazy_p(uint64_t b, uint64_t w, uint64_t wb, uint32_t m1)
+// formed as one IMAD.WIDE b0 w0, a three-input subtraction of q' (the third
+// input is the opaque zero: IADD3 / IADD3.X, never IMAD.X) and three IMADs
+// into the high word (m1 = -p1 mod 2^32): 2 IMAD.WIDE, 2 IMAD.HI and 3 IMAD.
+// Z selects how q' is subtracted: Z = true as a three-input add whose third
+// input is the opaque zero (IADD3 / IADD3.X on the ALU pipe -- the forward's
+// choice, where the multiply pipe binds), Z = false as the IMAD.WIDE addend
+// -q' (its negation may land on the multiply pipe as IMAD.X -- the inverse's
+// choice, where the ALU pipe is the fuller one; measured).
+template <bool Z>
+__device__ __forceinline__ uint64_t shoup_lazy_p(uint64_t b, uint64_t w, uint64_t wb, uint32_t m1, uint64_t zero)
 {
     uint64_t r;
-    asm("{\n\t"
-        ".reg .u32 b0, b1, v0, v1, w0, w1, t0, t1, q0, q1, r0, r1;\n\t"
-        ".reg .u64 q, a, t;\n\t"
-        "mov.b64 {b0, b1}, %1;\n\t"
-        "mov.b64 {w0, w1}, %2;\n\t"
-        "mov.b64 {v0, v1}, %3;\n\t"
-        "mul.hi.u32 t0, b1, v0;\n\t"
-        "mul.hi.u32 t1, b0, v1;\n\t"
-        "cvt.u64.u32 t, t0;\n\t"
-        "mad.wide.u32 q, b1, v1, t;\n\t"
-        "cvt.u64.u32 t, t1;\n\t"
-        "add.u64 q, q, t;\n\t"
-        "mov.b64 {q0, q1}, q;\n\t"
-        "sub.u64 q, 0, q;\n\t"
-        "mad.wide.u32 a, b0, w0, q;\n\t"
-        "mov.b64 {r0, r1}, a;\n\t"
-        "mad.lo.u32 r1, b0, w1, r1;\n\t"
-        "mad.lo.u32 r1, b1, w0, r1;\n\t"
-        "mad.lo.u32 r1, q0, %4, r1;\n\t"
-        "mov.b64 %0, {r0, r1};\n\t"
-        "}"
-        : "=l"(r)
-        : "l"(b), "l"(w), "l"(wb), "r"(m1));
+    if constexpr (Z) {
+        asm("{\n\t"
+            ".reg .u32 b0, b1, v0, v1, w0, w1, t0, t1, q0, q1, r0, r1;\n\t"
+            ".reg .u64 q, a, t;\n\t"
+            "mov.b64 {b0, b1}, %1;\n\t"
+            "mov.b64 {w0, w1}, %2;\n\t"
+            "mov.b64 {v0, v1}, %3;\n\t"
+            "mul.hi.u32 t0, b1, v0;\n\t"
+            "mul.hi.u32 t1, b0, v1;\n\t"
+            "cvt.u64.u32 t, t0;\n\t"
+            "mad.wide.u32 q, b1, v1, t;\n\t"
+            "cvt.u64.u32 t, t1;\n\t"
+            "add.u64 q, q, t;\n\t"
+            "mov.b64 {q0, q1}, q;\n\t"
+            "mul.wide.u32 a, b0, w0;\n\t"
+            "sub.u64 a, a, q;\n\t"
+            "add.u64 a, a, %5;\n\t"
+            "mov.b64 {r0, r1}, a;\n\t"
+            "mad.lo.u32 r1, b0, w1, r1;\n\t"
+            "mad.lo.u32 r1, b1, w0, r1;\n\t"
+            "mad.lo.u32 r1, q0, %4, r1;\n\t"
+            "mov.b64 %0, {r0, r1};\n\t"
+            "}"
+            : "=l"(r)
+            : "l"(b), "l"(w), "l"(wb), "r"(m1), "l"(zero));
+    } else {
+        asm("{\n\t"
+            ".reg .u32 b0, b1, v0, v1, w0, w1, t0, t1, q0, q1, r0, r1;\n\t"
+            ".reg .u64 q, a, t;\n\t"
+            "mov.b64 {b0, b1}, %1;\n\t"
+            "mov.b64 {w0, w1}, %2;\n\t"
+            "mov.b64 {v0, v1}, %3;\n\t"
+            "mul.hi.u32 t0, b1, v0;\n\t"
+            "mul.hi.u32 t1, b0, v1;\n\t"
+            "cvt.u64.u32 t, t0;\n\t"
+            "mad.wide.u32 q, b1, v1, t;\n\t"
+            "cvt.u64.u32 t, t1;\n\t"
+            "add.u64 q, q, t;\n\t"
+            "mov.b64 {q0, q1}, q;\n\t"
+            "sub.u64 q, 0, q;\n\t"
+            "mad.wide.u32 a, b0, w0, q;\n\t"
+            "mov.b64 {r0, r1}, a;\n\t"
+            "mad.lo.u32 r1, b0, w1, r1;\n\t"
+            "mad.lo.u32 r1, b1, w0, r1;\n\t"
+            "mad.lo.u32 r1, q0, %4, r1;\n\t"
+            "mov.b64 %0, {r0, r1};\n\t"
+            "}"
+            : "=l"(r)
+            : "l"(b), "l"(w), "l"(wb), "r"(m1));
+        (void)zero;
+    }
     return r;
 }
 
 // One Shoup multiply by a table twiddle, arithmetic chosen by the constants' type.
+// Z: see shoup_lazy_p (CT butterflies pass true, GS butterflies false).
+template <bool Z = false>
 __device__ __forceinline__ uint64_t shoup(uint64_t b, const Tw& t, const PrimeConst& c)
 {
     return shoup_lazy(b, t.w, t.wb, c.np);
 }
+template <bool Z = false>
 __device__ __forceinline__ uint64_t shoup(uint64_t b, const Tw& t, const PrimeConstP& c)
 {
-    return shoup_lazy_p(b, t.w, t.wb, c.m1);
+    return shoup_lazy_p<Z>(b, t.w, t.wb, c.m1, c.zero);
 }
 
 __device__ __forceinline__ uint64_t csub(uint64_t x, uint64_t m) { return x >= m ? x - m : x; }
@@ -200,35 +240,49 @@ struct TwMul;
 template <>
 struct TwMul<false> {
     Tw t;
-    template <class C>
+    template <bool Z = false, class C>
     __device__ __forceinline__ uint64_t mul(uint64_t x, const C& c) const
     {
-        return shoup(x, t, c);
+        return shoup<Z>(x, t, c);
     }
 };
 template <>
 struct TwMul<true> {
     Tw fine, coarse;
-    template <class C>
+    template <bool Z = false, class C>
     __device__ __forceinline__ uint64_t mul(uint64_t x, const C& c) const
     {
-        return shoup(shoup(x, fine, c), coarse, c);
+        return shoup<Z>(shoup<Z>(x, fine, c), coarse, c);
     }
 };
 
 // Cooley-Tukey butterfly (Algorithm 2) in Harvey's lazy form (R9),
-// widened for the [0,4p) multiplier: inputs and outputs in [0, 8p + 2^32).
-//   X <- X mod* 4p (< 4p + 2^32);  T = Y w (< 4p);  X' = X + T;  Y' = X - T + 4p.
+// widened for the [0,4p) multiplier (T = Y w < 4p for any Y < 2^64).
+//   red = 1 (any prime): inputs and outputs in [0, 8p + 2^32);
+//     X <- X mod* 4p (< 4p + 2^32);  X' = X + T;  Y' = X - T + 4p.
+//   red = 2 / 0 (Proth primes, p <= 2^60 - 2^32 + 1, so 16p + 2^32 < 2^64):
+//     the reduction runs on every other stage only -- the last stage of a
+//     kernel and every second one before it (ct_roundN), so every kernel's
+//     output and input stay below 12p + 2^32:
+//     red = 2: X <- X mod* 8p (< 8p + 2^32), outputs < 12p + 2^32;
+//     red = 0: no reduction, inputs < 12p + 2^32, outputs < 16p + 2^32.
+// The conditional subtraction is decided on the high words (csub_hi) and
+// folded into both outputs as 3-input adds (IADD3 / IADD3.X on the ALU pipe;
+// a 2-input 64-bit add lets ptxas emit IMAD.X on the multiply pipe).
 template <class W, class C>
-__device__ __forceinline__ void ct_bf(uint64_t& X, uint64_t& Y, const W& w, const C& c)
+__device__ __forceinline__ void ct_bf(uint64_t& X, uint64_t& Y, const W& w, const C& c, int red = 1)
 {
-    // the conditional subtraction folded into both outputs as 3-input adds
-    // (IADD3 / IADD3.X on the ALU pipe; a 2-input 64-bit add lets ptxas emit
-    // IMAD.X on the multiply pipe, the binding one)
-    const bool ge = (uint32_t)(X >> 32) > c.p4_hi;
-    const uint64_t s = ge ? c.p4 : 0, s2 = ge ? 0 : c.p4;
-    const uint64_t t = w.mul(Y, c);
     const uint64_t x = X;
+    if (red == 0) {
+        const uint64_t t = w.template mul<true>(Y, c);
+        X = x + t + c.zero;  // three inputs: IADD3 / IADD3.X, never IMAD.X
+        Y = x - t + c.p4;
+        return;
+    }
+    const bool ge = red == 2 ? (uint32_t)(x >> 32) > c.p8_hi : (uint32_t)(x >> 32) > c.p4_hi;
+    const uint64_t s = ge ? (red == 2 ? c.p8 : c.p4) : 0;
+    const uint64_t s2 = red == 2 ? (ge ? 0 - c.p4 : c.p4) : (ge ? 0 : c.p4);
+    const uint64_t t = w.template mul<true>(Y, c);
     X = x - s + t;
     Y = x - t + s2;
 }
@@ -356,6 +410,8 @@ __device__ __forceinline__ void ct_roundN(uint64_t (&x)[NI][16], uint32_t tib, u
 #pragma unroll
         for (int i = 0; i < Geo::r; ++i) {
             const int half = R >> (i + 1);
+            // Proth primes: reduce on the kernel's last stage and every second one before it
+            const int red = std::is_same_v<C, PrimeConstP> ? (((LOGM - 1 - (S + i)) & 1) ? 0 : 2) : 1;
 #pragma unroll
             for (int h = 0; h < (1 << i); ++h) {
                 const uint32_t idx = (B << i) + h;
@@ -364,13 +420,13 @@ __device__ __forceinline__ void ct_roundN(uint64_t (&x)[NI][16], uint32_t tib, u
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
 #pragma unroll
-                        for (int n = 0; n < NI; ++n) ct_bf(x[n][qd * R + k], x[n][qd * R + k + half], w, c);
+                        for (int n = 0; n < NI; ++n) ct_bf(x[n][qd * R + k], x[n][qd * R + k + half], w, c, red);
                 } else {
                     const TwMul<false> w{tabf(TwKey{idx, S + i, S, i, h, G / Geo::s})};
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
 #pragma unroll
-                        for (int n = 0; n < NI; ++n) ct_bf(x[n][qd * R + k], x[n][qd * R + k + half], w, c);
+                        for (int n = 0; n < NI; ++n) ct_bf(x[n][qd * R + k], x[n][qd * R + k + half], w, c, red);
                 }
             }
         }
