@@ -357,7 +357,7 @@ struct RoundGeo {
     static constexpr int s = (1 << LOGM) >> (S + r);
     static constexpr int GPT = SC::E / R;
     static constexpr int TB = SC::TB;
-    __device__ static __forceinline__ uint32_t elem(uint32_t G, int k)
+    __host__ __device__ static constexpr uint32_t elem(uint32_t G, int k)
     {
         const uint32_t g = G / s, o = G % s;
         return g * (R * s) + o + (uint32_t)k * s;
@@ -508,10 +508,20 @@ __device__ __forceinline__ uint64_t reduce_full(uint64_t x, const PrimeConst& c)
     const uint32_t q = __umulhi((uint32_t)(x >> 32), c.rn) >> 26;
     return csub(x - (uint64_t)q * c.p, c.p);
 }
-__device__ __forceinline__ uint64_t norm8(uint64_t x, const PrimeConst& c) { return reduce_full(x, c); }
+// Proth prime: q p = q + ((q p1) << 32) -- one IMAD instead of IMAD.WIDE + IMAD;
+// the subtraction of both terms is one three-input add.
+__device__ __forceinline__ uint64_t reduce_full(uint64_t x, const PrimeConstP& c)
+{
+    const uint32_t q = __umulhi((uint32_t)(x >> 32), c.rn) >> 26;
+    const uint32_t qp1 = q * (0u - c.m1);  // q p1 (mod 2^32): p1 = -m1
+    return csub(x - q - ((uint64_t)qp1 << 32), c.p);
+}
+template <class C>
+__device__ __forceinline__ uint64_t norm8(uint64_t x, const C& c) { return reduce_full(x, c); }
 // [0,4p) -> [0,p) (inverse outputs): two exact conditional subtractions, all
 // on the ALU pipe -- cheaper than reduce_full where the multiply pipe binds.
-__device__ __forceinline__ uint64_t norm4(uint64_t x, const PrimeConst& c) { return csub(csub(x, c.p2), c.p); }
+template <class C>
+__device__ __forceinline__ uint64_t norm4(uint64_t x, const C& c) { return csub(csub(x, c.p2), c.p); }
 
 // SMEM swizzle for contiguous blocks: XOR word-address bits 1..3 with
 // (bits 4..6 ^ bits 5..7).  16-byte pairs (2i, 2i+1) stay adjacent (vector
@@ -519,5 +529,28 @@ __device__ __forceinline__ uint64_t norm4(uint64_t x, const PrimeConst& c) { ret
 // or 128-bit ones in the stride-1 rounds -- is bank-conflict free
 // (DESIGN.md section 5.3).
 __device__ __forceinline__ uint32_t swz(uint32_t e) { return e ^ ((((e >> 4) ^ (e >> 5)) & 7u) << 1); }
+
+// Swizzled index of element k of a thread's group qd in one round, from the
+// thread's base sB = swz(elem(tib, 0)) (RoundGeo::elem):
+//   elem(qd TB + tib, k) = elem(tib, 0) + KS,  KS = elem(qd TB, k) a compile-time
+// constant whose bits are disjoint from elem(tib, 0)'s, and swz(e) = e ^ f(e)
+// with f linear over GF(2) in the bits of e -- so swz(B | KS) = sB ^ KS ^ f(KS).
+// When KS has no bit in 1..3 that is (sB ^ f(KS)) + KS: at most 8 distinct
+// LOP3s per round and immediate offsets, instead of a shift/mask/xor chain per
+// element.
+template <uint32_t KS>
+__device__ __forceinline__ uint32_t swz_at(uint32_t sB)
+{
+    constexpr uint32_t f = (((KS >> 4) ^ (KS >> 5)) & 7u) << 1;
+    if constexpr ((KS & 0xEu) == 0) {
+        if constexpr (f == 0) {
+            return sB + KS;
+        } else {
+            return (sB ^ f) + KS;
+        }
+    } else {
+        return sB ^ (KS ^ f);
+    }
+}
 
 }  // namespace ntt

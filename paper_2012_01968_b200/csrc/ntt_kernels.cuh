@@ -534,37 +534,45 @@ __global__ void __launch_bounds__(SharedCfg<LOGM>::CT, SharedCfg<LOGM>::MINB) k_
     };
 
     uint64_t x[16];
+    // element (qd, k) of the round at swz_at<elem(qd TB, k)>(swz(elem(tib, 0)))
     auto s_load = [&](auto ri) {
         using Geo = RoundGeo<LOGM, decltype(ri)::value, 4>;
-#pragma unroll
-        for (int qd = 0; qd < Geo::GPT; ++qd) {
+        const uint32_t sB = swz(Geo::elem(tib, 0));
+        static_for<Geo::GPT>([&](auto qdc) {
+            constexpr int qd = decltype(qdc)::value;
             if constexpr (Geo::s == 1 && Geo::R >= 2) {
-#pragma unroll
-                for (int k = 0; k < Geo::R; k += 2) {
-                    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k)));
+                static_for<Geo::R / 2>([&](auto kc) {
+                    constexpr int k = 2 * decltype(kc)::value;
+                    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(sb + swz_at<Geo::elem(qd * TB, k)>(sB));
                     x[qd * Geo::R + k] = v.x;
                     x[qd * Geo::R + k + 1] = v.y;
-                }
+                });
             } else {
-#pragma unroll
-                for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = sb[swz(Geo::elem(qd * TB + tib, k))];
+                static_for<Geo::R>([&](auto kc) {
+                    constexpr int k = decltype(kc)::value;
+                    x[qd * Geo::R + k] = sb[swz_at<Geo::elem(qd * TB, k)>(sB)];
+                });
             }
-        }
+        });
     };
     auto s_store = [&](auto ri) {
         using Geo = RoundGeo<LOGM, decltype(ri)::value, 4>;
-#pragma unroll
-        for (int qd = 0; qd < Geo::GPT; ++qd) {
+        const uint32_t sB = swz(Geo::elem(tib, 0));
+        static_for<Geo::GPT>([&](auto qdc) {
+            constexpr int qd = decltype(qdc)::value;
             if constexpr (Geo::s == 1 && Geo::R >= 2) {
-#pragma unroll
-                for (int k = 0; k < Geo::R; k += 2)
-                    *reinterpret_cast<ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k))) =
+                static_for<Geo::R / 2>([&](auto kc) {
+                    constexpr int k = 2 * decltype(kc)::value;
+                    *reinterpret_cast<ulonglong2*>(sb + swz_at<Geo::elem(qd * TB, k)>(sB)) =
                         make_ulonglong2(x[qd * Geo::R + k], x[qd * Geo::R + k + 1]);
+                });
             } else {
-#pragma unroll
-                for (int k = 0; k < Geo::R; ++k) sb[swz(Geo::elem(qd * TB + tib, k))] = x[qd * Geo::R + k];
+                static_for<Geo::R>([&](auto kc) {
+                    constexpr int k = decltype(kc)::value;
+                    sb[swz_at<Geo::elem(qd * TB, k)>(sB)] = x[qd * Geo::R + k];
+                });
             }
-        }
+        });
     };
     constexpr bool DIRECT0 = RoundGeo<LOGM, 0, 4>::s >= 16;
     static_assert(DIRECT0, "round 0 is read / written straight from global");
@@ -593,16 +601,18 @@ __global__ void __launch_bounds__(SharedCfg<LOGM>::CT, SharedCfg<LOGM>::MINB) k_
             s_store(ri);
             block_sync<TB>(blk);
         });
-        if (active) {
-#pragma unroll
-            for (int j = 0; j < E / 2; ++j) {
-                const uint32_t ch = j * TB + tib;
-                *reinterpret_cast<ulonglong2*>(g + 2 * ch) = *reinterpret_cast<const ulonglong2*>(sb + swz(2 * ch));
-            }
+        if (active) {  // 128-bit coalesced stores; word 2 ch = 2 j TB + 2 tib
+            const uint32_t s2 = swz(2 * tib);
+            static_for<E / 2>([&](auto jc) {
+                constexpr int j = decltype(jc)::value;
+                *reinterpret_cast<ulonglong2*>(g + 2 * (j * TB + tib)) =
+                    *reinterpret_cast<const ulonglong2*>(sb + swz_at<2 * j * TB>(s2));
+            });
         }
     } else {
-#pragma unroll
-        for (int j = 0; j < E / 2; ++j) {
+        const uint32_t s2 = swz(2 * tib);
+        static_for<E / 2>([&](auto jc) {
+            constexpr int j = decltype(jc)::value;
             const uint32_t ch = j * TB + tib;
             ulonglong2 v = *reinterpret_cast<const ulonglong2*>(g + 2 * ch);
             if constexpr (MUL) {  // fused NTT-domain product (ntt_pointwise_inverse)
@@ -610,8 +620,8 @@ __global__ void __launch_bounds__(SharedCfg<LOGM>::CT, SharedCfg<LOGM>::MINB) k_
                 v.x = mont_mul(u.x, v.x, pc);
                 v.y = mont_mul(u.y, v.y, pc);
             }
-            *reinterpret_cast<ulonglong2*>(sb + swz(2 * ch)) = v;
-        }
+            *reinterpret_cast<ulonglong2*>(sb + swz_at<2 * j * TB>(s2)) = v;
+        });
         twiddles_ready();
         static_for<NR>([&](auto rj) {
             constexpr int RI = NR - 1 - decltype(rj)::value;

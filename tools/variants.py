@@ -27,10 +27,11 @@ ap.add_argument("--steps", type=int, default=10)
 ap.add_argument("--ot", action="store_true")
 ap.add_argument("--log-n1", type=int, default=0)
 ap.add_argument("--variants", default="4,4;3,3;4,3;3,4")
+ap.add_argument("--primes", default="proth", choices=["2n", "proth"])
 a = ap.parse_args()
 logn, L, B, _ = CONFIGS[a.config]
 N = 1 << logn
-primes = find_primes(N, L)
+primes = find_primes(N, L, a.primes)
 x = synth.rns_rows(primes, B, N, config_id=synth.CONFIG_IDS[a.config])
 host = torch.from_numpy(x.view(np.int64))
 d = host.cuda()
