@@ -8,10 +8,16 @@
 //              over stride-N2 columns, a 16-column tile per CTA so every global
 //              access is a full 128-byte row segment (coalescing),
 //              twiddles Psi[0..N1) preloaded into SMEM.
-//   k_contig : Kernel-2 / Kernel-2' -- contiguous N2-point blocks -- and the
-//              single-kernel path for N <= 2^13, where one CTA holds whole rows.
-//              Optional on-the-fly twiddling on the last (forward)
-//              or first (inverse) 1-2 stages.
+//   k_shared : Kernel-2 / Kernel-2' (default) -- contiguous N2-point blocks,
+//              one CTA per (prime, block position, 2^12/N2 ciphertexts), the
+//              block position's twiddles staged once in SMEM.
+//   k_blocks : Kernel-2 / Kernel-2', persistent and cp.async-pipelined (small
+//              batches, and tuning knob 5).
+//   k_contig : the single-kernel path for N <= 2^13, where one CTA holds whole
+//              rows (and one-shot Kernel-2 variants, knobs 3/4).
+//   k_cols_pipe : persistent pipelined Kernel-1 (knob 5).
+//   Optional on-the-fly twiddling on the last (forward) or first
+//   (inverse) 1-2 stages of the kernel that holds them.
 //
 // Both run per-thread radix-2^LOGE register NTTs with SMEM exchanges between
 // rounds; 64-bit words, Shoup modmul.
@@ -58,9 +64,6 @@ __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>
     uint64_t* col = a.data + (((uint64_t)b * a.L + l) << LOGN) + tile * 16u + c;
     const Tw* tab = a.tab + ((uint64_t)l << LOGN);
     const PCT pc = load_pc<PCT>(a.pc, l);
-
-    for (uint32_t i = tid; i < (uint32_t)M; i += CT) tws[i] = ldg_tw(tab + i);  // Psi[0..N1)
-    __syncthreads();
     auto tabf = [&](const TwKey& k) { return tws[k.idx]; };
     auto otf = [&](uint32_t) { return TwMul<true>{}; };  // OT never reaches Kernel-1
 
@@ -103,11 +106,19 @@ __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>
         }
     };
 
+    // Psi[0..N1) into SMEM, issued after round 0's global loads so
+    // the two DRAM round trips overlap
+    auto preload_twiddles = [&]() {
+        for (uint32_t i = tid; i < (uint32_t)M; i += CT) tws[i] = ldg_tw(tab + i);
+        __syncthreads();
+    };
+
     if constexpr (!INV) {
         static_for<NR>([&](auto ri) {
             constexpr int RI = decltype(ri)::value;
             if constexpr (RI == 0) {
                 g_load(ri);
+                preload_twiddles();
             } else {
                 s_load(ri);
             }
@@ -125,6 +136,7 @@ __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>
             using RC = std::integral_constant<int, RI>;
             if constexpr (RI == NR - 1) {
                 g_load(RC{});
+                preload_twiddles();
             } else {
                 s_load(RC{});
             }
@@ -1054,9 +1066,14 @@ cudaError_t launch_k2_t(bool inverse, int loge, const KArgs& a, int ots, uint32_
 {
     using namespace detail;
     const int logm = (int)(a.logn - a.log_n1);
-    if (loge == 7)  // shared-twiddle Kernel-2 (radix 16, one CTA per block position x 256/TB ciphertexts)
+    // shared-twiddle Kernel-2 (radix 16, one CTA per block position x 256/TB
+    // ciphertexts) when the batch fills its CTAs (NB = 2^12 / N2 ciphertexts);
+    // smaller batches (e.g. the C5 request stream, batch 1) take the persistent
+    // pipelined Kernel-2, whose warps walk blocks of any row
+    if (loge == 7 && a.batch >= (4096u >> logm))
         return inverse ? shared_switch<true, PCT>(logm, a, ots, st, K2Sizes{})
                        : shared_switch<false, PCT>(logm, a, ots, st, K2Sizes{});
+    if (loge == 7) loge = 5;
     if (loge == 5)  // pipelined persistent Kernel-2 (radix 16)
         return inverse ? blocks_switch<4, true, PCT>(logm, a, ots, st, K2Sizes{})
                        : blocks_switch<4, false, PCT>(logm, a, ots, st, K2Sizes{});

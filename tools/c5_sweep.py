@@ -24,12 +24,14 @@ from paper_2012_01968_b200 import Plan, find_primes  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--depth", type=int, default=64)
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--fused", action="store_true", help="single-pass cluster kernel (ntt_opts_t.fused = 1)")
 a = ap.parse_args()
 N = 1 << 16
-all_primes = find_primes(N, 45)
+ap_primes = os.environ.get("C5_PRIMES", "proth")
+all_primes = find_primes(N, 45, ap_primes)
 for L in (1, 2, 4, 8, 15, 30, 45):
     primes = all_primes[:L]
-    plan = Plan(N, primes)
+    plan = Plan(N, primes, fused=True if a.fused else None)
     x = synth.rns_rows(primes, 1, N, config_id=synth.CONFIG_IDS["C5"])
     reqs = torch.from_numpy(np.repeat(x, a.depth, axis=0).view(np.int64)).cuda()  # depth requests
     one = reqs[:1]
@@ -64,5 +66,5 @@ for L in (1, 2, 4, 8, 15, 30, 45):
     batched_us = e[0].elapsed_time(e[1]) * 1e3 / a.depth
     print(json.dumps({"config": "C5", "N": N, "L": L, "latency_us_median": round(float(np.median(lat)), 2),
                       "stream_us_per_request": round(stream_us, 2), "batched_us_per_request": round(batched_us, 2),
-                      "depth": a.depth}), flush=True)
+                      "depth": a.depth, "primes": ap_primes, "fused": a.fused}), flush=True)
     plan.close()
