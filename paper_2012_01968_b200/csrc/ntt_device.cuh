@@ -130,83 +130,48 @@ __device__ __forceinline__ uint64_t shoup_lazy(uint64_t b, uint64_t w, uint64_t 
 // Shoup's modmul for a Proth prime p = p1 2^32 + 1: the same truncated
 // quotient q' (so the same [0, 4p) output bound), and
 //   r = b w - q' p = lo64(b w) - q' - (q0' p1 << 32)  (mod 2^64),
-// formed as one IMAD.WIDE b0 w0, a three-input subtraction of q' (the third
-// input is the opaque zero: IADD3 / IADD3.X, never IMAD.X) and three IMADs
-// into the high word (m1 = -p1 mod 2^32): 2 IMAD.WIDE, 2 IMAD.HI and 3 IMAD.
-// Z selects how q' is subtracted: Z = true as a three-input add whose third
-// input is the opaque zero (IADD3 / IADD3.X on the ALU pipe -- the forward's
-// choice, where the multiply pipe binds), Z = false as the IMAD.WIDE addend
-// -q' (its negation may land on the multiply pipe as IMAD.X -- the inverse's
-// choice, where the ALU pipe is the fuller one; measured).
-template <bool Z>
-__device__ __forceinline__ uint64_t shoup_lazy_p(uint64_t b, uint64_t w, uint64_t wb, uint32_t m1, uint64_t zero)
+// formed as one IMAD.WIDE b0 w0 with the addend -q' and three IMADs into the
+// high word (m1 = -p1 mod 2^32): 2 IMAD.WIDE, 2 IMAD.HI and 3 IMAD.  (A
+// variant subtracting q' as a three-input add with an opaque zero, which
+// keeps the negation off the multiply pipe, measured 1-2 % slower in the
+// kernels and 5 % in tools/bf_roof -- DESIGN.md 5.1.)
+__device__ __forceinline__ uint64_t shoup_lazy_p(uint64_t b, uint64_t w, uint64_t wb, uint32_t m1)
 {
     uint64_t r;
-    if constexpr (Z) {
-        asm("{\n\t"
-            ".reg .u32 b0, b1, v0, v1, w0, w1, t0, t1, q0, q1, r0, r1;\n\t"
-            ".reg .u64 q, a, t;\n\t"
-            "mov.b64 {b0, b1}, %1;\n\t"
-            "mov.b64 {w0, w1}, %2;\n\t"
-            "mov.b64 {v0, v1}, %3;\n\t"
-            "mul.hi.u32 t0, b1, v0;\n\t"
-            "mul.hi.u32 t1, b0, v1;\n\t"
-            "cvt.u64.u32 t, t0;\n\t"
-            "mad.wide.u32 q, b1, v1, t;\n\t"
-            "cvt.u64.u32 t, t1;\n\t"
-            "add.u64 q, q, t;\n\t"
-            "mov.b64 {q0, q1}, q;\n\t"
-            "mul.wide.u32 a, b0, w0;\n\t"
-            "sub.u64 a, a, q;\n\t"
-            "add.u64 a, a, %5;\n\t"
-            "mov.b64 {r0, r1}, a;\n\t"
-            "mad.lo.u32 r1, b0, w1, r1;\n\t"
-            "mad.lo.u32 r1, b1, w0, r1;\n\t"
-            "mad.lo.u32 r1, q0, %4, r1;\n\t"
-            "mov.b64 %0, {r0, r1};\n\t"
-            "}"
-            : "=l"(r)
-            : "l"(b), "l"(w), "l"(wb), "r"(m1), "l"(zero));
-    } else {
-        asm("{\n\t"
-            ".reg .u32 b0, b1, v0, v1, w0, w1, t0, t1, q0, q1, r0, r1;\n\t"
-            ".reg .u64 q, a, t;\n\t"
-            "mov.b64 {b0, b1}, %1;\n\t"
-            "mov.b64 {w0, w1}, %2;\n\t"
-            "mov.b64 {v0, v1}, %3;\n\t"
-            "mul.hi.u32 t0, b1, v0;\n\t"
-            "mul.hi.u32 t1, b0, v1;\n\t"
-            "cvt.u64.u32 t, t0;\n\t"
-            "mad.wide.u32 q, b1, v1, t;\n\t"
-            "cvt.u64.u32 t, t1;\n\t"
-            "add.u64 q, q, t;\n\t"
-            "mov.b64 {q0, q1}, q;\n\t"
-            "sub.u64 q, 0, q;\n\t"
-            "mad.wide.u32 a, b0, w0, q;\n\t"
-            "mov.b64 {r0, r1}, a;\n\t"
-            "mad.lo.u32 r1, b0, w1, r1;\n\t"
-            "mad.lo.u32 r1, b1, w0, r1;\n\t"
-            "mad.lo.u32 r1, q0, %4, r1;\n\t"
-            "mov.b64 %0, {r0, r1};\n\t"
-            "}"
-            : "=l"(r)
-            : "l"(b), "l"(w), "l"(wb), "r"(m1));
-        (void)zero;
-    }
+    asm("{\n\t"
+        ".reg .u32 b0, b1, v0, v1, w0, w1, t0, t1, q0, q1, r0, r1;\n\t"
+        ".reg .u64 q, a, t;\n\t"
+        "mov.b64 {b0, b1}, %1;\n\t"
+        "mov.b64 {w0, w1}, %2;\n\t"
+        "mov.b64 {v0, v1}, %3;\n\t"
+        "mul.hi.u32 t0, b1, v0;\n\t"
+        "mul.hi.u32 t1, b0, v1;\n\t"
+        "cvt.u64.u32 t, t0;\n\t"
+        "mad.wide.u32 q, b1, v1, t;\n\t"
+        "cvt.u64.u32 t, t1;\n\t"
+        "add.u64 q, q, t;\n\t"
+        "mov.b64 {q0, q1}, q;\n\t"
+        "sub.u64 q, 0, q;\n\t"
+        "mad.wide.u32 a, b0, w0, q;\n\t"
+        "mov.b64 {r0, r1}, a;\n\t"
+        "mad.lo.u32 r1, b0, w1, r1;\n\t"
+        "mad.lo.u32 r1, b1, w0, r1;\n\t"
+        "mad.lo.u32 r1, q0, %4, r1;\n\t"
+        "mov.b64 %0, {r0, r1};\n\t"
+        "}"
+        : "=l"(r)
+        : "l"(b), "l"(w), "l"(wb), "r"(m1));
     return r;
 }
 
 // One Shoup multiply by a table twiddle, arithmetic chosen by the constants' type.
-// Z: see shoup_lazy_p (CT butterflies pass true, GS butterflies false).
-template <bool Z = false>
 __device__ __forceinline__ uint64_t shoup(uint64_t b, const Tw& t, const PrimeConst& c)
 {
     return shoup_lazy(b, t.w, t.wb, c.np);
 }
-template <bool Z = false>
 __device__ __forceinline__ uint64_t shoup(uint64_t b, const Tw& t, const PrimeConstP& c)
 {
-    return shoup_lazy_p<Z>(b, t.w, t.wb, c.m1, c.zero);
+    return shoup_lazy_p(b, t.w, t.wb, c.m1);
 }
 
 __device__ __forceinline__ uint64_t csub(uint64_t x, uint64_t m) { return x >= m ? x - m : x; }
@@ -240,19 +205,19 @@ struct TwMul;
 template <>
 struct TwMul<false> {
     Tw t;
-    template <bool Z = false, class C>
+    template <class C>
     __device__ __forceinline__ uint64_t mul(uint64_t x, const C& c) const
     {
-        return shoup<Z>(x, t, c);
+        return shoup(x, t, c);
     }
 };
 template <>
 struct TwMul<true> {
     Tw fine, coarse;
-    template <bool Z = false, class C>
+    template <class C>
     __device__ __forceinline__ uint64_t mul(uint64_t x, const C& c) const
     {
-        return shoup<Z>(shoup<Z>(x, fine, c), coarse, c);
+        return shoup(shoup(x, fine, c), coarse, c);
     }
 };
 
@@ -274,7 +239,7 @@ __device__ __forceinline__ void ct_bf(uint64_t& X, uint64_t& Y, const W& w, cons
 {
     const uint64_t x = X;
     if (red == 0) {
-        const uint64_t t = w.template mul<true>(Y, c);
+        const uint64_t t = w.mul(Y, c);
         X = x + t + c.zero;  // three inputs: IADD3 / IADD3.X, never IMAD.X
         Y = x - t + c.p4;
         return;
@@ -282,7 +247,7 @@ __device__ __forceinline__ void ct_bf(uint64_t& X, uint64_t& Y, const W& w, cons
     const bool ge = red == 2 ? (uint32_t)(x >> 32) > c.p8_hi : (uint32_t)(x >> 32) > c.p4_hi;
     const uint64_t s = ge ? (red == 2 ? c.p8 : c.p4) : 0;
     const uint64_t s2 = red == 2 ? (ge ? 0 - c.p4 : c.p4) : (ge ? 0 : c.p4);
-    const uint64_t t = w.template mul<true>(Y, c);
+    const uint64_t t = w.mul(Y, c);
     X = x - s + t;
     Y = x - t + s2;
 }
