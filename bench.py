@@ -49,17 +49,29 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def alu_peak(form: str = "2n"):
-    """Derived integer roof: the IMAD pipe issues 16
-    lanes/clk/SMSP for IMAD and 8 for IMAD.WIDE/IMAD.HI (measured,
-    profiles/r01_alu_roof.jsonl); a 64-bit Shoup butterfly needs at least
-    4 wide + 1 hi (full q) ... we count the floor our kernels target:
-    q' = 1 WIDE + 2 HI, r = 2 WIDE + 4 IMAD -> 5 x 4 + 4 x 2 = 28 IMAD-pipe
-    clk per warp-butterfly per SMSP.  148 SMs x 4 SMSP x 32 / 28 per clk."""
+# Multiply-pipe cost of one warp-instruction per SMSP, in clocks: IMAD from the
+# guide (rt_SMSP = 2); IMAD.WIDE / IMAD.HI measured on B200 with independent
+# chains (profiles/r01_alu_roof.jsonl: 24 and 28 per clk per SM; confirmed by
+# the 2 WIDE + 2 HI + 3 IMAD mix at 25.7 clk, profiles/r01g_bf_roof_variants.txt).
+CLK_IMAD, CLK_WIDE, CLK_HI = 2.0, 16 / 3.0, 32 / 7.0
+
+
+def alu_floor_clk(form: str = "2n") -> float:
+    """Multiply-pipe clocks per warp-butterfly of the truncated-quotient Shoup
+    butterfly: general primes 3 WIDE + 2 HI + 4 IMAD, Proth
+    primes 2 WIDE + 2 HI + 3 IMAD."""
+    if form == "proth":
+        return 2 * CLK_WIDE + 2 * CLK_HI + 3 * CLK_IMAD
+    return 3 * CLK_WIDE + 2 * CLK_HI + 4 * CLK_IMAD
+
+
+def alu_peak(form: str = "2n", nominal: bool = False):
+    """Derived integer roof in G butterflies/s: 148 SMs x 4 SMSPs x 32 lanes /
+    (clk per warp-butterfly) x 1.965 GHz.  nominal=True uses quarter-rate
+    (4 clk) WIDE/HI instead of the measured rates (an upper bound)."""
     sm_clk_ghz = 1.965
-    # Proth primes (p = 1 mod 2^32): r = 1 WIDE + 3 IMAD -> 4 x 4 + 3 x 2 = 22 clk
-    bfly_per_clk = 148 * 4 * 32 / (22.0 if form == "proth" else 28.0)
-    return bfly_per_clk * sm_clk_ghz  # G butterflies / s
+    clk = (22.0 if form == "proth" else 28.0) if nominal else alu_floor_clk(form)
+    return 148 * 4 * 32 / clk * sm_clk_ghz
 
 
 # ------------------------------------------------------------------ clocks
@@ -284,7 +296,8 @@ def run_own(args):
         st = logn
     bfly_per_launch = rows * (N // 2) * st
     achieved = bfly_per_launch / (dom_ms * 1e-3) / 1e9
-    peak = alu_peak(args.primes if info.get("proth") else "2n")
+    form = args.primes if info.get("proth") else "2n"
+    peak = alu_peak(form)
     dom_bytes = 2 * 8 * N * rows  # compulsory bytes of one pass: read + write every word
     hbm_dom = dom_bytes / (dom_ms * 1e-3) / 1e9
     traffic = None
@@ -392,7 +405,9 @@ def run_own(args):
             "roofline": {
                 "bound": "alu", "kernel": dom, "achieved": round(achieved, 1), "peak": round(peak, 1),
                 "unit": "Gbutterfly/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                "peak_kind": "derived from IMAD-pipe rates x 148 SMs x 1.965 GHz (DESIGN.md 7)",
+                "peak_kind": "derived: multiply-pipe clk per Shoup butterfly (IMAD 2 clk per guide; IMAD.WIDE 5.33, "
+                             "IMAD.HI 4.57 clk measured) x 148 SMs x 1.965 GHz (DESIGN.md 7)",
+                "peak_nominal_quarter_rate": round(alu_peak(form, nominal=True), 1),
                 "hbm": {"achieved": round(hbm_dom, 1), "peak": hbm_peak, "unit": "GB/s",
                         "frac": round(hbm_dom / hbm_peak, 4), "peak_kind": peak_kind,
                         "bytes": "compulsory 16N per row per pass"},
