@@ -342,6 +342,16 @@ struct K2Layout {
         for (int i = 0; i < SC::NR && SC::S(i) < S; ++i) off += ((1u << SC::r(i)) - 1u) << SC::S(i);
         return off;
     }
+    // Entries [0, used(OTS)) hold the twiddles of the stages below LOGM - OTS;
+    // the last OTS stages (the tail of the last round, OTS <= its r) come from
+    // on-the-fly twiddling and their entries are never read -- a
+    // kernel under OT copies only this prefix (3/4 of the table saved at OTS = 2).
+    __host__ __device__ static constexpr uint32_t used(int OTS)
+    {
+        if (OTS == 0) return 1u << LOGM;
+        const int Sl = SC::S(SC::NR - 1), i0 = LOGM - OTS - Sl;
+        return round_off(Sl) + (((1u << i0) - 1u) << Sl);
+    }
 };
 
 // Forward round: r Cooley-Tukey stages on each of the thread's GPT groups.

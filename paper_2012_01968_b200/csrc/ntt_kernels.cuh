@@ -531,9 +531,10 @@ __global__ void __launch_bounds__(SharedCfg<LOGM>::CT, SharedCfg<LOGM>::MINB) k_
     const Tw* ot = a.ot + (uint64_t)l * (B_ot + ((1u << a.logn) >> a.ot_logb));
     const PCT pc = load_pc<PCT>(a.pc, l);
 
-    {  // the block position's twiddle segment, once per CTA
+    {  // the block position's twiddle segment, once per CTA (under OT only the prefix of the table stages)
         const Tw* t2 = a.tab2 + ((uint64_t)l << a.logn) + ((uint64_t)bb << LOGM);
-        for (uint32_t i = tid; i < (uint32_t)M; i += CT) cp_async16(tws + i, t2 + i);
+        constexpr uint32_t USED = K2Layout<LOGM, 4>::used(OTS);
+        for (uint32_t i = tid; i < USED; i += CT) cp_async16(tws + i, t2 + i);
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
     uint64_t* sb = sm + blk * M;
@@ -717,8 +718,10 @@ __global__ void __launch_bounds__(PipeCfg<LOGM, LOGE>::CT, PipeCfg<LOGM, LOGE>::
         if (gb < a.total_blocks) {
             const uint32_t bb = gb & n1mask, q = gb >> a.log_n1, l = q / a.batch;
             const Tw* t2 = a.tab2 + ((uint64_t)l << a.logn) + ((uint64_t)bb << LOGM);
+            constexpr uint32_t USED = K2Layout<LOGM, LOGE>::used(OTS);  // OT stages' entries are not read
 #pragma unroll
-            for (int j = 0; j < E; ++j) cp_async16(tws + j * TB + tib, t2 + j * TB + tib);
+            for (int j = 0; j < E; ++j)
+                if (j * TB + tib < USED) cp_async16(tws + j * TB + tib, t2 + j * TB + tib);
         }
     };
     auto commit = [] { asm volatile("cp.async.commit_group;" ::: "memory"); };
