@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(FusedCfg::CT, 2) k_fused(const KArgs a)
         for (int u = 0; u < NI; ++u)
 #pragma unroll
             for (int kk = 0; kk < C; ++kk) xc[u][kk] = g[col(u) + ((uint64_t)kk << LOGM)];
-        ct_roundN<LOGC, LOGC, 0, NOOT, NI>(xc, 0u, 0u, tabc, otf, pc);
+        ct_roundN<LOGC, LOGC, 0, NOOT, NI, true>(xc, 0u, 0u, tabc, otf, pc);
         cluster_wait();
         // ---- scatter: word (j, kk) -> CTA kk, position j
 #pragma unroll

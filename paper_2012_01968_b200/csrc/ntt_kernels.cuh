@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>
             } else {
                 s_load(ri);
             }
-            ct_round<LOGN1, LOGE, RI, 1 << 20>(x, tib, 0u, tabf, otf, pc);
+            ct_round<LOGN1, LOGE, RI, 1 << 20, true>(x, tib, 0u, tabf, otf, pc);
             if constexpr (RI == NR - 1) {
                 g_store(ri);  // [0, 8p): Kernel-2 continues the lazy chain
             } else {
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(ColsPipeCfg<LOGN1, LOGE>::CT, ColsPipeCfg<LOGN
             static_for<NR>([&](auto ri) {
                 constexpr int RI = decltype(ri)::value;
                 s_load(ri);
-                ct_round<LOGN1, LOGE, RI, 1 << 20>(x, tib, 0u, tabf, otf, pc);
+                ct_round<LOGN1, LOGE, RI, 1 << 20, true>(x, tib, 0u, tabf, otf, pc);
                 if constexpr (RI == NR - 1) {
                     g_store(ri);
                 } else {
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
                 } else {
                     s_load(ri);
                 }
-                ct_round<LOGM, LOGE, RI, OT_FROM>(x, tib, F - 1u, tabf, otf, pc);
+                ct_round<LOGM, LOGE, RI, OT_FROM, !TWS>(x, tib, F - 1u, tabf, otf, pc);  // single kernel: canonical input
                 if constexpr (RI == NR - 1) {
 #pragma unroll
                     for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // [0,8p+2^32) -> [0,p)
