@@ -19,8 +19,9 @@ import synth  # noqa: E402
 from paper_2012_01968_b200 import Plan  # noqa: E402
 
 
-def run(N, L, batch, **kw):
-    primes = oracle.find_primes(N, L)
+def run(N, L, batch, proth=False, **kw):
+    # Proth primes (p = 1 mod 2^32) from the oracle's own scan at step 2^32
+    primes = oracle.find_primes(1 << 31, L) if proth else oracle.find_primes(N, L)
     psis = [oracle.find_psi(p, N) for p in primes]
     x = synth.rns_rows(primes, batch, N, config_id=14)
     plan = Plan(N, primes, **kw)
@@ -44,7 +45,10 @@ def run(N, L, batch, **kw):
 
 
 cases = [(1 << 10, 2, 1, {}), (1 << 12, 1, 1, {"ot": True}), (1 << 14, 2, 1, {}), (1 << 15, 2, 1, {"ot": True}),
-         (1 << 16, 1, 1, {"log_n1": 8})]
+         (1 << 16, 1, 1, {"log_n1": 8}),
+         # shared-twiddle Kernel-2 (batch >= 2^12 / N2), Proth kernels, the single-pass cluster kernel
+         (1 << 14, 1, 16, {}), (1 << 17, 1, 8, {"proth": True}), (1 << 16, 1, 8, {"proth": True, "ot": True}),
+         (1 << 12, 1, 2, {"proth": True}), (1 << 15, 1, 1, {"fused": True}), (1 << 17, 1, 1, {"fused": True, "proth": True})]
 bad = [c[:3] for c in cases if not run(*c[:3], **c[3])]
 print("sanitize workload:", "ok" if not bad else f"MISMATCH {bad}")
 sys.exit(1 if bad else 0)
