@@ -335,3 +335,28 @@ def test_fused_option_errors():
     N = 1 << 16
     with pytest.raises(NttError):
         Plan(N, chain(N, 1)[0], fused=True, ot=True)
+
+
+@pytest.mark.parametrize("form", ["proth", "2n"])
+def test_fused_full_size_c4_sampled(form):
+    """The single-pass cluster kernel at BASELINE.json's full C4 size (N=2^17,
+    60 primes, batch 32) in the launch configuration bench.py would time with
+    fused=True: 48 sampled rows against the oracle, and the exact roundtrip of
+    every row."""
+    from paper_2012_01968_b200 import find_primes as lib_find_primes
+    N, L, B = 1 << 17, 60, 32
+    primes = lib_find_primes(N, L, form)
+    assert primes == (oracle.find_primes(1 << 31, L) if form == "proth" else oracle.find_primes(N, L))
+    x = synth.rns_rows(primes, B, N, config_id=synth.CONFIG_IDS["C4"])
+    plan = Plan(N, primes, fused=True)
+    assert plan.info()["passes"] == 1 and plan.info()["cluster"] == 16
+    d = to_dev(x)
+    plan.forward(d)
+    got = to_host(d)
+    rng = np.random.default_rng(7)
+    for r in rng.choice(B * L, 48, replace=False):
+        b, l = divmod(int(r), L)
+        want = oracle.ntt_forward(x[b, l].copy(), primes[l], oracle.find_psi(primes[l], N))
+        assert np.array_equal(got[b, l], want), (b, l)
+    plan.inverse(d)
+    assert np.array_equal(to_host(d), x)

@@ -203,6 +203,48 @@ def test_find_primes_properties(logn, count):
         expect_next -= 2 * N
 
 
+def test_find_proth_primes_properties():
+    """R18: the oracle's own scan at step 2^32 (N = 2^31) yields descending
+    primes p = k 2^32 + 1 in [2^59, 2^60); every skipped candidate in between
+    is composite (a factor is exhibited), every kept one passes Fermat tests."""
+    ps = oracle.find_primes(1 << 31, 64)
+    step = 1 << 32
+    rng = random.Random(31)
+    expect_next = ((P60 - 2) // step) * step + 1
+    for p in ps:
+        assert (1 << 59) <= p < P60 and p % step == 1 and p % (1 << 18) == 1
+        for _ in range(8):
+            a = rng.randrange(2, p - 1)
+            assert pow(a, p - 1, p) == 1
+        while expect_next > p:
+            f = pollard_rho(expect_next)
+            assert 1 < f < expect_next and expect_next % f == 0
+            expect_next -= step
+        assert expect_next == p
+        expect_next -= step
+
+
+def test_closed_forms_full_size_proth():
+    """The closed forms of test_closed_forms_full_size at N = 2^17 for a Proth
+    prime (the bench's default family): delta_j and constant inputs."""
+    N, logn = 1 << 17, 17
+    p = oracle.find_primes(1 << 31, 3)[2]
+    psi = oracle.find_psi(p, N)
+    assert pow(psi, N, p) == p - 1
+    rng = random.Random(18)
+    idx = rng.sample(range(N), 48) + [0, N - 1]
+    j = rng.randrange(N)
+    a = np.zeros(N, dtype=np.uint64)
+    a[j] = 1
+    out = oracle.ntt_forward(a, p, psi)
+    for i in idx:
+        assert int(out[i]) == pow(psi, j * (2 * brev(i, logn) + 1), p)
+    c = rng.randrange(1, p)
+    out = oracle.ntt_forward(np.full(N, c, dtype=np.uint64), p, psi)
+    for i in idx:
+        assert int(out[i]) == 2 * c * pow(1 - pow(psi, 2 * brev(i, logn) + 1, p), -1, p) % p
+
+
 def test_find_primes_range_exhausted():
     with pytest.raises(ValueError):
         oracle.find_primes(4, 10, 17, 128)
