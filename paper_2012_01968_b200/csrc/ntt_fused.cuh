@@ -71,7 +71,7 @@ struct FusedCfg {
 template <int LOGC, bool INV, class PCT>
 __global__ void __launch_bounds__(FusedCfg::CT, 2) k_fused(const KArgs a)
 {
-    constexpr int LOGM = FusedCfg::LOGM, M = 1 << LOGM, C = 1 << LOGC, CT = FusedCfg::CT;
+    constexpr int LOGM = FusedCfg::LOGM, C = 1 << LOGC, CT = FusedCfg::CT;
     constexpr int NI = 16 / C;  // columns per thread
     using SC = Sched<LOGM, 4>;
     static_assert(SC::TB == CT, "one block per CTA");

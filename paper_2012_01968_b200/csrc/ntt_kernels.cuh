@@ -499,20 +499,22 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
 // N2 = 2^9) that synchronise among themselves only.  256 threads, 64 registers:
 // 4 CTAs = 32 warps per SM, like Kernel-1, so the multiply pipe is fed by
 // occupancy rather than by a software pipeline.
-template <int LOGM>
+template <int LOGM, bool INV = false>
 struct SharedCfg {
     static constexpr int TB = Sched<LOGM, 4>::TB;
     static constexpr int CT = 256;
     static constexpr int NB = CT / TB;  // blocks (ciphertexts) per CTA
     static constexpr size_t SMEM = (size_t)NB * (8u << LOGM) + (sizeof(Tw) << LOGM);
-    static constexpr int MINB = 4;
+    // measured on C4: the forward (final reduction, more live values) runs
+    // faster with 85 registers at 3 CTAs/SM, the inverse with 64 at 4
+    static constexpr int MINB = INV ? 4 : 3;
 };
 
 template <int LOGM, bool INV, int OTS, bool MUL = false, class PCT = PrimeConst>
-__global__ void __launch_bounds__(SharedCfg<LOGM>::CT, SharedCfg<LOGM>::MINB) k_shared(const KArgs a)
+__global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>::MINB) k_shared(const KArgs a)
 {
     using SC = Sched<LOGM, 4>;
-    using CC = SharedCfg<LOGM>;
+    using CC = SharedCfg<LOGM, INV>;
     constexpr int M = SC::M, E = SC::E, TB = SC::TB, NR = SC::NR, NB = CC::NB, CT = CC::CT;
     constexpr int OT_FROM = OTS ? LOGM - OTS : (1 << 20);
     extern __shared__ __align__(16) uint64_t sm[];
@@ -919,7 +921,7 @@ cudaError_t launch_blocks_t(KArgs a, cudaStream_t st)
 template <int LOGM, bool INV, int OTS, bool MUL, class PCT>
 cudaError_t launch_shared_t(const KArgs& a, cudaStream_t st)
 {
-    using CC = SharedCfg<LOGM>;
+    using CC = SharedCfg<LOGM, INV>;
     auto fn = k_shared<LOGM, INV, OTS, MUL, PCT>;
     static std::atomic<uint64_t> attr_set{0};  // one bit per device
     if (!set_once(attr_set)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
