@@ -374,8 +374,11 @@ struct TwKey {
 // load serves NI times the butterflies, and NI independent chains add ILP.
 // CANON: the kernel's input is canonical ([0, p): Kernel-1 and the single-CTA
 // kernel), so with Proth primes the reductions of local stages 0 and 1 are
-// skipped (their inputs stay below 9p).
-template <int LOGM, int LOGE, int RI, int OT_FROM, int NI, bool CANON = false, class TabF, class OtF, class C>
+// skipped (their inputs stay below 9p).  FINAL: the kernel normalises its
+// output with reduce_full (valid for any word), so the reduction pattern is
+// shifted by one stage and the last stage needs none (outputs < 16p + 2^32).
+template <int LOGM, int LOGE, int RI, int OT_FROM, int NI, bool CANON = false, bool FINAL = false, class TabF,
+          class OtF, class C>
 __device__ __forceinline__ void ct_roundN(uint64_t (&x)[NI][16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
                                           const OtF& otf, const C& c)
 {
@@ -390,7 +393,7 @@ __device__ __forceinline__ void ct_roundN(uint64_t (&x)[NI][16], uint32_t tib, u
             const int half = R >> (i + 1);
             // Proth primes: reduce on the kernel's last stage and every second one before it
             const int red = std::is_same_v<C, PrimeConstP>
-                                ? ((((LOGM - 1 - (S + i)) & 1) || (CANON && S + i < 2)) ? 0 : 2)
+                                ? ((((LOGM - 1 - (S + i) - (FINAL ? 1 : 0)) & 1) || (CANON && S + i < 2)) ? 0 : 2)
                                 : 1;
 #pragma unroll
             for (int h = 0; h < (1 << i); ++h) {
@@ -413,11 +416,13 @@ __device__ __forceinline__ void ct_roundN(uint64_t (&x)[NI][16], uint32_t tib, u
     }
 }
 
-template <int LOGM, int LOGE, int RI, int OT_FROM, bool CANON = false, class TabF, class OtF, class C>
+template <int LOGM, int LOGE, int RI, int OT_FROM, bool CANON = false, bool FINAL = false, class TabF, class OtF,
+          class C>
 __device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
                                          const OtF& otf, const C& c)
 {
-    ct_roundN<LOGM, LOGE, RI, OT_FROM, 1, CANON>(reinterpret_cast<uint64_t(&)[1][16]>(x), tib, Fm1, tabf, otf, c);
+    ct_roundN<LOGM, LOGE, RI, OT_FROM, 1, CANON, FINAL>(reinterpret_cast<uint64_t(&)[1][16]>(x), tib, Fm1, tabf,
+                                                       otf, c);
 }
 
 // Inverse round: the same groups and twiddle indices, Gentleman-Sande stages

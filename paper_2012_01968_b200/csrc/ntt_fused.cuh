@@ -158,10 +158,10 @@ __global__ void __launch_bounds__(FusedCfg::CT, 2) k_fused(const KArgs a)
         static_for<NR>([&](auto ri) {
             constexpr int RI = decltype(ri)::value;
             s_load(ri);
-            ct_round<LOGM, 4, RI, NOOT>(x, tid, Fm1, tab2f, otf, pc);
+            ct_round<LOGM, 4, RI, NOOT, false, true>(x, tid, Fm1, tab2f, otf, pc);
             if constexpr (RI == NR - 1) {
 #pragma unroll
-                for (int kk = 0; kk < 16; ++kk) x[kk] = norm8(x[kk], pc);  // [0,8p+2^32) -> [0,p)
+                for (int kk = 0; kk < 16; ++kk) x[kk] = norm8(x[kk], pc);  // any word -> [0,p)
             }
             s_store(ri);
             __syncthreads();

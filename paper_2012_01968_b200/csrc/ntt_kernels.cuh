@@ -453,10 +453,10 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
                 } else {
                     s_load(ri);
                 }
-                ct_round<LOGM, LOGE, RI, OT_FROM, !TWS>(x, tib, F - 1u, tabf, otf, pc);  // single kernel: canonical input
+                ct_round<LOGM, LOGE, RI, OT_FROM, !TWS, true>(x, tib, F - 1u, tabf, otf, pc);  // single kernel: canonical input
                 if constexpr (RI == NR - 1) {
 #pragma unroll
-                    for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // [0,8p+2^32) -> [0,p)
+                    for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // any word (lazy < 16p + 2^32) -> [0,p)
                 }
                 s_store(ri);
                 block_sync<TB>(blk);
@@ -608,10 +608,10 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
         static_for<NR>([&](auto ri) {
             constexpr int RI = decltype(ri)::value;
             if constexpr (RI > 0) s_load(ri);
-            ct_round<LOGM, 4, RI, OT_FROM>(x, tib, Fm1, tabf, otf, pc);
+            ct_round<LOGM, 4, RI, OT_FROM, false, true>(x, tib, Fm1, tabf, otf, pc);
             if constexpr (RI == NR - 1) {
 #pragma unroll
-                for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // [0,8p+2^32) -> [0,p)
+                for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // any word (lazy < 16p + 2^32) -> [0,p)
             }
             s_store(ri);
             block_sync<TB>(blk);
@@ -800,10 +800,10 @@ __global__ void __launch_bounds__(PipeCfg<LOGM, LOGE>::CT, PipeCfg<LOGM, LOGE>::
             static_for<NR>([&](auto ri) {
                 constexpr int RI = decltype(ri)::value;
                 s_load(ri);
-                ct_round<LOGM, LOGE, RI, OT_FROM>(x, tib, Fm1, tabf, otf, pc);
+                ct_round<LOGM, LOGE, RI, OT_FROM, false, true>(x, tib, Fm1, tabf, otf, pc);
                 if constexpr (RI == NR - 1) {
 #pragma unroll
-                    for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // [0,8p+2^32) -> [0,p)
+                    for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // any word (lazy < 16p + 2^32) -> [0,p)
                 }
                 s_store(ri);
                 block_sync<TB>(blk);
