@@ -380,6 +380,10 @@ def run_own(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_ok = bool(torch.equal(out_host, host))
+    if world > 1:  # every rank's exactness flags to rank 0 (NCCL carries verification, not data)
+        t = torch.tensor([int(ok_roundtrip), int(e2e_ok)], device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        ok_roundtrip, e2e_ok = bool(t[0].item()), bool(t[1].item())
     del ws
 
     cpu = None
