@@ -522,11 +522,16 @@ ntt_status_t ntt_forward_variant(ntt_plan_t plan, uint64_t* data, unsigned batch
     return ntt::launch_baseline_forward((int)variant, a, (cudaStream_t)stream) == cudaSuccess ? NTT_OK : NTT_ERR_CUDA;
 }
 
+// pipeline slots (stream + device buffer) of the host-buffer executor: with
+// three, chunk k's H2D, chunk k-1's transforms and chunk k-2's D2H overlap
+// without a slot waiting for its own previous D2H
+static constexpr unsigned kHostSlots = 3;
+
 static unsigned auto_chunk(const ntt_plan_s* plan, unsigned batch, unsigned chunk)
 {
     if (chunk) return std::min(chunk, batch);
     const uint64_t ct_bytes = (uint64_t)plan->L * 8ull << plan->logn;
-    uint64_t c = std::max<uint64_t>(1, (128ull << 20) / ct_bytes);  // ~128 MiB per pipeline step
+    uint64_t c = std::max<uint64_t>(1, (64ull << 20) / ct_bytes);  // ~64 MiB per pipeline step
     return (unsigned)std::min<uint64_t>(c, batch);
 }
 
@@ -534,7 +539,8 @@ uint64_t ntt_workspace_words(ntt_plan_t plan, unsigned batch, unsigned chunk)
 {
     if (!plan || batch == 0) return 0;
     const unsigned c = auto_chunk(plan, batch, chunk);
-    const unsigned nbuf = c < batch ? 2 : 1;
+    const unsigned steps = (batch + c - 1) / c;
+    const unsigned nbuf = std::min<unsigned>(kHostSlots, steps);
     return (uint64_t)nbuf * c * plan->L << plan->logn;
 }
 
@@ -549,18 +555,19 @@ ntt_status_t ntt_execute_host(ntt_plan_t plan, unsigned flags, const uint64_t* h
     if (workspace_words < ntt_workspace_words(plan, batch, c)) return NTT_ERR_INVALID_ARG;
     DeviceGuard g(plan->device);
     const uint64_t ct_words = (uint64_t)plan->L << plan->logn;
-    cudaStream_t st[2];
-    if (cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking) != cudaSuccess) return NTT_ERR_CUDA;
-    if (cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking) != cudaSuccess) {
-        cudaStreamDestroy(st[0]);
-        return NTT_ERR_CUDA;
-    }
+    const unsigned nslot = std::min<unsigned>(kHostSlots, (batch + c - 1) / c);
+    cudaStream_t st[kHostSlots] = {};
+    for (unsigned i = 0; i < nslot; ++i)
+        if (cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking) != cudaSuccess) {
+            for (unsigned j = 0; j < i; ++j) cudaStreamDestroy(st[j]);
+            return NTT_ERR_CUDA;
+        }
     cudaError_t e = cudaSuccess;
     unsigned k = 0;
     for (unsigned b0 = 0; b0 < batch && e == cudaSuccess; b0 += c, ++k) {
         const unsigned nb = std::min(c, batch - b0);
-        cudaStream_t sk = st[k & 1];
-        uint64_t* buf = workspace + (uint64_t)(k & 1) * c * ct_words;
+        cudaStream_t sk = st[k % nslot];
+        uint64_t* buf = workspace + (uint64_t)(k % nslot) * c * ct_words;
         const size_t bytes = (size_t)nb * ct_words * 8;
         e = cudaMemcpyAsync(buf, host_in + (uint64_t)b0 * ct_words, bytes, cudaMemcpyHostToDevice, sk);
         if (e == cudaSuccess && (flags & NTT_DIR_FORWARD)) e = enqueue(plan, buf, nb, false, sk);
@@ -568,9 +575,12 @@ ntt_status_t ntt_execute_host(ntt_plan_t plan, unsigned flags, const uint64_t* h
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(host_out + (uint64_t)b0 * ct_words, buf, bytes, cudaMemcpyDeviceToHost, sk);
     }
-    cudaError_t e0 = cudaStreamSynchronize(st[0]), e1 = cudaStreamSynchronize(st[1]);
-    cudaStreamDestroy(st[0]);
-    cudaStreamDestroy(st[1]);
+    cudaError_t e0 = cudaSuccess, e1 = cudaSuccess;
+    for (unsigned i = 0; i < nslot; ++i) {
+        const cudaError_t ei = cudaStreamSynchronize(st[i]);
+        if (ei != cudaSuccess) e0 = ei;
+        cudaStreamDestroy(st[i]);
+    }
     if (e == cudaSuccess) e = e0 != cudaSuccess ? e0 : e1;
     return e == cudaSuccess ? NTT_OK : NTT_ERR_CUDA;
 }
