@@ -147,13 +147,15 @@ def my_shard(rank: int, G: int, L: int, batch_per_gpu: int):
 
 # ------------------------------------------------------------------ reference arm
 
-def cpu_oracle_sample(logn: int, L_total: int, ciphertexts: int, config_id: int):
+def cpu_oracle_sample(logn: int, L_total: int, ciphertexts: int, config_id: int, form: str = "proth"):
     """Time the oracle (as it stands) on `ciphertexts` full-L ciphertexts
-    (fwd+inv) on all host cores.  Returns (us_per_ntt_intt, seconds, cores)."""
+    (fwd+inv) on all host cores, with the same prime family as the GPU arm
+    (the oracle's own scans: step 2N for "2n", step 2^32 for "proth").
+    Returns (us_per_ntt_intt, seconds, cores)."""
     import oracle
     import synth
     N = 1 << logn
-    primes = oracle.find_primes(N, L_total)
+    primes = oracle.find_primes(1 << 31, L_total) if form == "proth" else oracle.find_primes(N, L_total)
     psis = [oracle.find_psi(p, N) for p in primes]
     x = synth.rns_rows(primes, ciphertexts, N, config_id=config_id)
     cores = len(os.sched_getaffinity(0))
@@ -172,11 +174,11 @@ def run_reference(args):
     import synth
     cfg_id = synth.CONFIG_IDS[args.config]
     for _ in range(args.warmup):
-        cpu_oracle_sample(logn, L, 1, cfg_id)
+        cpu_oracle_sample(logn, L, 1, cfg_id, args.primes)
     times = []
     cores = None
     for _ in range(args.steps):
-        us, dt, cores = cpu_oracle_sample(logn, L, 1, cfg_id)
+        us, dt, cores = cpu_oracle_sample(logn, L, 1, cfg_id, args.primes)
         times.append(dt)
     T = sum(times) / len(times)
     value = T * 1e6  # one full-L ciphertext per step
@@ -388,7 +390,7 @@ def run_own(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        us, dt, cores = cpu_oracle_sample(logn, L_total, 1, cfg_id)
+        us, dt, cores = cpu_oracle_sample(logn, L_total, 1, cfg_id, args.primes)
         cpu = {"value": round(us, 1), "unit": "us", "cores": cores, "kind": "oracle",
                "sample": f"1 ciphertext x {L_total} primes x N=2^{logn}, fwd+inv ({dt:.2f} s)"}
 
