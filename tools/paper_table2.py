@@ -1,8 +1,8 @@
 """The paper's Table 2 setting on B200: forward NTT of np = 21
 residue rows (batch 1) at N = 2^14..2^17 with the radix-2 baseline, the
 register radix-16 kernel, and the two-kernel SMEM path without / with OT.
-Prints one JSON line per N with times (us, all 21 rows together, as in the
-paper, R13) and the SMEM+OT / radix-2 speedup the paper reports as
+Prints one JSON line per N with GPU times (us, all 21 rows together, as in the
+paper, R13; calls replayed from a CUDA graph) and the SMEM+OT / radix-2 speedup the paper reports as
 4.2x on Titan V.
 
     python tools/paper_table2.py [--reps 50]
@@ -31,13 +31,25 @@ a = ap.parse_args()
 
 
 def time_us(fn, d, reps):
+    """GPU time per call: `reps` calls captured in one CUDA graph and replayed,
+    so host launch cost (several us per C-ABI call, larger than the kernels at
+    these sizes) stays out of the measurement."""
     for _ in range(5):
         fn(d)
     torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                fn(d)
+    torch.cuda.current_stream().wait_stream(s)
+    g.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(reps):
-        fn(d)
+    g.replay()
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) * 1e3 / reps
