@@ -202,7 +202,10 @@ struct Contig32Cfg {
     static constexpr int NB = CT / TB;
 };
 
-template <int LOGM, bool INV, bool FUSE0, bool K2>
+// SHARED (Kernel-2 only, batch >= NB): one CTA per (prime, block position,
+// NB ciphertexts) -- the blocks of a CTA share their twiddles, staged in SMEM
+// once (the 64-bit k_shared design).
+template <int LOGM, bool INV, bool FUSE0, bool K2, bool SHARED = false>
 __global__ void __launch_bounds__(Contig32Cfg<LOGM>::CT, Contig32Cfg<LOGM>::CT > 256 ? 1 : 2) k32_contig(const KArgs32 a)
 {
     using SC = Sched<LOGM, 4>;
@@ -211,17 +214,37 @@ __global__ void __launch_bounds__(Contig32Cfg<LOGM>::CT, Contig32Cfg<LOGM>::CT >
     const uint32_t tid = threadIdx.x, blk = tid / TB, tib = tid % TB;
     uint32_t* sb = sm32 + blk * M;
     const uint32_t n1mask = (1u << a.log_n1) - 1u;
-    uint32_t gb = blockIdx.x * NB + blk;
-    const bool active = gb < a.total_blocks;
-    if (!active) gb = a.total_blocks - 1;
-    const uint32_t bb = gb & n1mask, q = gb >> a.log_n1;
-    const uint32_t l = q / a.batch, b = q - l * a.batch;
+    uint32_t bb, l, b;
+    bool active;
+    if constexpr (SHARED) {
+        const uint32_t groups = (a.batch + NB - 1) / NB;
+        const uint32_t cg = blockIdx.x % groups, rest = blockIdx.x / groups;
+        bb = rest & n1mask;
+        l = rest >> a.log_n1;
+        b = cg * NB + blk;
+        active = b < a.batch;
+        if (!active) b = 0;
+    } else {
+        uint32_t gb = blockIdx.x * NB + blk;
+        active = gb < a.total_blocks;
+        if (!active) gb = a.total_blocks - 1;
+        bb = gb & n1mask;
+        const uint32_t q = gb >> a.log_n1;
+        l = q / a.batch;
+        b = q - l * a.batch;
+    }
     uint32_t* g = a.data + (((uint64_t)b * a.L + l) << a.logn) + (uint64_t)bb * M;
     const PrimeConst32 pc = a.pc[l];
     const Tw32* tab = a.tab + ((uint64_t)l << a.logn);
     const Tw32* tb2 = K2 ? a.tab2 + ((uint64_t)l << a.logn) + ((uint64_t)bb << LOGM) : nullptr;
+    Tw32* const tws = reinterpret_cast<Tw32*>(sm32 + NB * M);  // SHARED: the block position's segment
+    if constexpr (SHARED) {
+        for (uint32_t i = tid; i < (uint32_t)M; i += Contig32Cfg<LOGM>::CT) tws[i] = ldg_tw(tb2 + i);
+    }
     auto tabf = [&](const TwKey& k) {
-        if constexpr (K2)
+        if constexpr (SHARED)
+            return tws[K2Layout<LOGM, 4>::round_off(k.S) + ((((1u << k.i) - 1u + k.h) << k.S) + k.g)];
+        else if constexpr (K2)
             return ldg_tw(tb2 + K2Layout<LOGM, 4>::round_off(k.S) + ((((1u << k.i) - 1u + k.h) << k.S) + k.g));
         else
             return ldg_tw(tab + k.idx);
@@ -317,15 +340,17 @@ cudaError_t launch32_cols_t(const KArgs32& a, uint32_t rows, cudaStream_t st)
     return cudaPeekAtLastError();
 }
 
-template <int LOGM, bool INV, bool FUSE0, bool K2>
+template <int LOGM, bool INV, bool FUSE0, bool K2, bool SHARED>
 cudaError_t launch32_contig_t(const KArgs32& a, cudaStream_t st)
 {
     using CC = w32::Contig32Cfg<LOGM>;
-    const size_t smem = (size_t)CC::NB * (1 << LOGM) * 4;
-    auto fn = w32::k32_contig<LOGM, INV, FUSE0, K2>;
+    const size_t smem = (size_t)CC::NB * (1 << LOGM) * 4 + (SHARED ? sizeof(Tw32) << LOGM : 0);
+    auto fn = w32::k32_contig<LOGM, INV, FUSE0, K2, SHARED>;
     static std::atomic<uint64_t> attr{0};
     if (!set_once32(attr)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    fn<<<(a.total_blocks + CC::NB - 1) / CC::NB, CC::CT, smem, st>>>(a);
+    const uint32_t grid = SHARED ? (a.L << a.log_n1) * ((a.batch + CC::NB - 1) / CC::NB)
+                                 : (a.total_blocks + CC::NB - 1) / CC::NB;
+    fn<<<grid, CC::CT, smem, st>>>(a);
     return cudaPeekAtLastError();
 }
 
@@ -333,7 +358,13 @@ template <bool INV, bool FUSE0, bool K2, int... Ls>
 cudaError_t contig32_switch(int logm, const KArgs32& a, cudaStream_t st, std::integer_sequence<int, Ls...>)
 {
     cudaError_t err = cudaErrorInvalidValue;
-    ((logm == Ls ? (err = launch32_contig_t<Ls, INV, FUSE0, K2>(a, st), 0) : 0), ...);
+    // Kernel-2 with a batch that fills the CTA: the shared-twiddle form
+    const bool shared = K2 && a.batch >= (4096u >> logm);  // NB = 256 / (N2 / 16) ciphertexts per CTA
+    ((logm == Ls ? (err = shared ? launch32_contig_t<Ls, INV, FUSE0, K2, K2>(a, st)
+                                 : launch32_contig_t<Ls, INV, FUSE0, K2, false>(a, st),
+                    0)
+                 : 0),
+     ...);
     return err;
 }
 

@@ -25,6 +25,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C4")
 ap.add_argument("--steps", type=int, default=10)
 ap.add_argument("--log-n1", type=int, default=0)
+ap.add_argument("--primes", default="proth", choices=["2n", "proth"], help="64-bit prime family")
 a = ap.parse_args()
 logn, L, B, _ = CONFIGS[a.config]
 N = 1 << logn
@@ -50,7 +51,7 @@ def timeit(plan, d, steps):
 
 for bits in (64, 32):
     nl = L if bits == 64 else 2 * L
-    primes = find_primes(N, nl) if bits == 64 else find_primes32(N, nl)
+    primes = find_primes(N, nl, a.primes) if bits == 64 else find_primes32(N, nl)
     x = synth.rns_rows(primes, B, N, config_id=synth.CONFIG_IDS.get(a.config, 15))
     if bits == 64:
         d = torch.from_numpy(x.view(np.int64)).cuda()
