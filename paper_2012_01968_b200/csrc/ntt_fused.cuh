@@ -65,13 +65,13 @@ __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.w
 struct FusedCfg {
     static constexpr int LOGM = 13;            // words per CTA: 2^13 (64 KiB)
     static constexpr int CT = 512;             // threads per CTA, 16 words each
-    static constexpr size_t SMEM = (size_t)8 << LOGM;
+    static constexpr size_t SMEM = ((size_t)8 << LOGM) + 16 * sizeof(Tw);  // block + Psi[0..C) (C <= 16)
 };
 
 template <int LOGC, bool INV, class PCT>
 __global__ void __launch_bounds__(FusedCfg::CT, 2) k_fused(const KArgs a)
 {
-    constexpr int LOGM = FusedCfg::LOGM, C = 1 << LOGC, CT = FusedCfg::CT;
+    constexpr int LOGM = FusedCfg::LOGM, M = 1 << LOGM, C = 1 << LOGC, CT = FusedCfg::CT;
     constexpr int NI = 16 / C;  // columns per thread
     using SC = Sched<LOGM, 4>;
     static_assert(SC::TB == CT, "one block per CTA");
@@ -89,8 +89,13 @@ __global__ void __launch_bounds__(FusedCfg::CT, 2) k_fused(const KArgs a)
     const PCT pc = load_pc<PCT>(a.pc, l);
     const uint32_t Fm1 = C + k - 1;  // block k of the split N = C x 2^13: F = C + k
 
-    // column phase twiddles Psi[1..C): every column of every CTA uses them (broadcast loads)
-    auto tabc = [&](const TwKey& t) { return ldg_tw(tab + t.idx); };
+    // column phase twiddles Psi[1..C): every column of every CTA uses them; staged
+    // in SMEM behind the block (loading them from global inside the round let
+    // ptxas hoist all C-1 pairs into registers and spill)
+    Tw* const twc = reinterpret_cast<Tw*>(sm + M);
+    if (tid < (uint32_t)C) twc[tid] = ldg_tw(tab + tid);
+    __syncthreads();
+    auto tabc = [&](const TwKey& t) { return twc[t.idx]; };
     // block phase twiddles: Kernel-2 order (K2Layout), contiguous across the lanes of a warp
     auto tab2f = [&](const TwKey& t) {
         return ldg_tw(tb2 + K2Layout<LOGM, 4>::round_off(t.S) + ((((1u << t.i) - 1u + t.h) << t.S) + t.g));
