@@ -56,6 +56,22 @@ __device__ __forceinline__ Tw32 ldg_tw(const Tw32* p)
 // (bits 5..7 ^ bits 6..8); conflict-free for every round pattern of M >= 2^9
 // (scalar and 128-bit accesses; half-warp bank model over this XOR family).
 __device__ __forceinline__ uint32_t swz32(uint32_t e) { return e ^ ((((e >> 5) ^ (e >> 6)) & 7u) << 2); }
+// swz32 of (base | KS) from sB = swz32(base), KS a compile-time offset with bits
+// disjoint from base's (the 64-bit swz_at argument, ntt_device.cuh)
+template <uint32_t KS>
+__device__ __forceinline__ uint32_t swz32_at(uint32_t sB)
+{
+    constexpr uint32_t f = (((KS >> 5) ^ (KS >> 6)) & 7u) << 2;
+    if constexpr ((KS & 0x1Cu) == 0) {
+        if constexpr (f == 0) {
+            return sB + KS;
+        } else {
+            return (sB ^ f) + KS;
+        }
+    } else {
+        return sB ^ (KS ^ f);
+    }
+}
 
 // Rounds (same geometry and twiddle algebra as the 64-bit engine).
 template <int LOGM, int LOGE, int RI, class TabF>
@@ -129,8 +145,11 @@ __global__ void __launch_bounds__((1 << LOGN1) * 2, LOGN1 >= 9 ? 1 : 2) k32_cols
     uint32_t* col = a.data + (((uint64_t)b * a.L + l) << LOGN) + tile * 32u + c;
     const Tw32* tab = a.tab + ((uint64_t)l << LOGN);
     const PrimeConst32 pc = a.pc[l];
-    for (uint32_t i = tid; i < (uint32_t)M; i += CT) tws[i] = ldg_tw(tab + i);
-    __syncthreads();
+    // Psi[0..N1) into SMEM, issued after round 0's global loads (the two DRAM round trips overlap)
+    auto preload_twiddles = [&]() {
+        for (uint32_t i = tid; i < (uint32_t)M; i += CT) tws[i] = ldg_tw(tab + i);
+        __syncthreads();
+    };
     auto tabf = [&](const TwKey& k) { return tws[k.idx]; };
 
     uint32_t x[16];
@@ -165,7 +184,12 @@ __global__ void __launch_bounds__((1 << LOGN1) * 2, LOGN1 >= 9 ? 1 : 2) k32_cols
     if constexpr (!INV) {
         static_for<NR>([&](auto ri) {
             constexpr int RI = decltype(ri)::value;
-            if constexpr (RI == 0) g_io(ri, false); else s_io(ri, false);
+            if constexpr (RI == 0) {
+                g_io(ri, false);
+                preload_twiddles();
+            } else {
+                s_io(ri, false);
+            }
             ct_round<LOGN1, 4, RI>(x, tib, tabf, pc);
             if constexpr (RI == NR - 1) {
                 g_io(ri, true);
@@ -178,7 +202,12 @@ __global__ void __launch_bounds__((1 << LOGN1) * 2, LOGN1 >= 9 ? 1 : 2) k32_cols
         static_for<NR>([&](auto rj) {
             constexpr int RI = NR - 1 - decltype(rj)::value;
             using RC = std::integral_constant<int, RI>;
-            if constexpr (RI == NR - 1) g_io(RC{}, false); else s_io(RC{}, false);
+            if constexpr (RI == NR - 1) {
+                g_io(RC{}, false);
+                preload_twiddles();
+            } else {
+                s_io(RC{}, false);
+            }
             gs_round<LOGN1, 4, RI, true>(x, tib, tabf, pc);
             if constexpr (RI == 0) {
 #pragma unroll
@@ -205,8 +234,12 @@ struct Contig32Cfg {
 // SHARED (Kernel-2 only, batch >= NB): one CTA per (prime, block position,
 // NB ciphertexts) -- the blocks of a CTA share their twiddles, staged in SMEM
 // once (the 64-bit k_shared design).
+#ifndef NTT32_K2_MINB
+#define NTT32_K2_MINB 4  // 64 registers, 4 CTAs / 32 warps per SM (measured 2 % faster than 2)
+#endif
 template <int LOGM, bool INV, bool FUSE0, bool K2, bool SHARED = false>
-__global__ void __launch_bounds__(Contig32Cfg<LOGM>::CT, Contig32Cfg<LOGM>::CT > 256 ? 1 : 2) k32_contig(const KArgs32 a)
+__global__ void __launch_bounds__(Contig32Cfg<LOGM>::CT,
+                                  Contig32Cfg<LOGM>::CT > 256 ? 1 : (K2 ? NTT32_K2_MINB : 2)) k32_contig(const KArgs32 a)
 {
     using SC = Sched<LOGM, 4>;
     constexpr int M = SC::M, E = SC::E, TB = SC::TB, NR = SC::NR, NB = Contig32Cfg<LOGM>::NB;
@@ -264,18 +297,21 @@ __global__ void __launch_bounds__(Contig32Cfg<LOGM>::CT, Contig32Cfg<LOGM>::CT >
     __syncthreads();
 
     uint32_t x[16];
+    // element (qd, k) at swz32_at<elem(qd TB, k)>(swz32(elem(tib, 0))): one base per round
     auto s_io = [&](auto ri, bool store) {
         using Geo = RoundGeo<LOGM, decltype(ri)::value, 4>;
-#pragma unroll
-        for (int qd = 0; qd < Geo::GPT; ++qd)
-#pragma unroll
-            for (int k = 0; k < Geo::R; ++k) {
-                const uint32_t e = Geo::elem(qd * TB + tib, k);
+        const uint32_t sB = swz32(Geo::elem(tib, 0));
+        static_for<Geo::GPT>([&](auto qdc) {
+            constexpr int qd = decltype(qdc)::value;
+            static_for<Geo::R>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                const uint32_t a = swz32_at<Geo::elem(qd * TB, k)>(sB);
                 if (store)
-                    sb[swz32(e)] = x[qd * Geo::R + k];
+                    sb[a] = x[qd * Geo::R + k];
                 else
-                    x[qd * Geo::R + k] = sb[swz32(e)];
-            }
+                    x[qd * Geo::R + k] = sb[a];
+            });
+        });
     };
     if constexpr (!INV) {
         static_for<NR>([&](auto ri) {
