@@ -15,9 +15,10 @@ import synth  # noqa: E402
 from paper_2012_01968_b200 import Plan, find_primes, _native  # noqa: E402
 
 N = 1 << 16
+FUSED = "--fused" in sys.argv
 for L in (1, 8, 45):
     primes = find_primes(N, L, "proth")
-    plan = Plan(N, primes)
+    plan = Plan(N, primes, fused=True if FUSED else None)
     x = torch.from_numpy(synth.rns_rows(primes, 1, N, config_id=synth.CONFIG_IDS["C5"]).view(np.int64)).cuda()
     ref = x.clone()
     for _ in range(5):
@@ -68,7 +69,7 @@ for L in (1, 8, 45):
     e[1].record()
     torch.cuda.synchronize()
     ok = bool(torch.equal(x, ref))
-    print(json.dumps({"N": N, "L": L, "host_us_per_call_binding": round(py_us, 2), "host_us_per_call_cabi": round(c_us, 2),
+    print(json.dumps({"N": N, "L": L, "fused": FUSED, "host_us_per_call_binding": round(py_us, 2), "host_us_per_call_cabi": round(c_us, 2),
                       "graph_latency_us": round(float(np.median(lat)), 2),
                       "graph_stream_us_per_request": round(e[0].elapsed_time(e[1]) * 1e3 / 64, 2), "ok": ok}), flush=True)
     plan.close()
