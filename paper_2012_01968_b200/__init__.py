@@ -63,11 +63,17 @@ def _dev_ptr(t, N: int, L: int, bits: int = 64) -> tuple[int, int]:
     return t.data_ptr(), t.numel() // (N * L)
 
 
-def _stream_handle(stream) -> int:
+def _stream_handle(stream, t=None) -> int:
+    """cudaStream_t of `stream`, or of the current stream of t's device (the
+    raw-stream query is several us cheaper than torch.cuda.current_stream())."""
     import torch
 
     if stream is None:
-        stream = torch.cuda.current_stream()
+        dev = t.device.index if t is not None else torch.cuda.current_device()
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        if raw is not None:
+            return raw(dev)
+        stream = torch.cuda.current_stream(dev)
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
@@ -117,13 +123,13 @@ class Plan:
     def forward(self, x, stream=None):
         """In-place forward NTT of a CUDA [batch][L][N] tensor (asynchronous)."""
         ptr, batch = _dev_ptr(x, self.N, self.L)
-        check(lib().ntt_forward(self.handle, ptr, batch, _stream_handle(stream)), "ntt_forward")
+        check(lib().ntt_forward(self.handle, ptr, batch, _stream_handle(stream, x)), "ntt_forward")
         return x
 
     def inverse(self, x, stream=None):
         """In-place inverse NTT of a CUDA [batch][L][N] tensor (asynchronous)."""
         ptr, batch = _dev_ptr(x, self.N, self.L)
-        check(lib().ntt_inverse(self.handle, ptr, batch, _stream_handle(stream)), "ntt_inverse")
+        check(lib().ntt_inverse(self.handle, ptr, batch, _stream_handle(stream, x)), "ntt_inverse")
         return x
 
     @property
@@ -134,7 +140,7 @@ class Plan:
     def launch_pass(self, x, direction: int, pass_index: int, stream=None):
         """Enqueue one kernel of a direction (for per-kernel timing)."""
         ptr, batch = _dev_ptr(x, self.N, self.L)
-        check(lib().ntt_launch_pass(self.handle, ptr, batch, direction, pass_index, _stream_handle(stream)),
+        check(lib().ntt_launch_pass(self.handle, ptr, batch, direction, pass_index, _stream_handle(stream, x)),
               "ntt_launch_pass")
         return x
 
@@ -144,7 +150,7 @@ class Plan:
         ptr, batch = _dev_ptr(x, self.N, self.L)
         if batch_a != batch:
             raise ValueError("operands must have the same batch")
-        check(lib().ntt_pointwise_inverse(self.handle, pa, ptr, batch, _stream_handle(stream)),
+        check(lib().ntt_pointwise_inverse(self.handle, pa, ptr, batch, _stream_handle(stream, x)),
               "ntt_pointwise_inverse")
         return x
 
@@ -154,14 +160,14 @@ class Plan:
         pb, batch = _dev_ptr(b, self.N, self.L)
         if batch_a != batch:
             raise ValueError("operands must have the same batch")
-        check(lib().ntt_negacyclic_mul(self.handle, pa, pb, batch, _stream_handle(stream)), "ntt_negacyclic_mul")
+        check(lib().ntt_negacyclic_mul(self.handle, pa, pb, batch, _stream_handle(stream, b)), "ntt_negacyclic_mul")
         return b
 
     def forward_variant(self, x, variant: int, stream=None):
         """Forward NTT through one of the paper's comparison kernels
         (1 = radix-2 per stage, 2 = register radix-16; 0 = default path)."""
         ptr, batch = _dev_ptr(x, self.N, self.L)
-        check(lib().ntt_forward_variant(self.handle, ptr, batch, variant, _stream_handle(stream)),
+        check(lib().ntt_forward_variant(self.handle, ptr, batch, variant, _stream_handle(stream, x)),
               "ntt_forward_variant")
         return x
 
@@ -237,12 +243,12 @@ class Plan32:
 
     def forward(self, x, stream=None):
         ptr, batch = _dev_ptr(x, self.N, self.L, 32)
-        check(lib().ntt_forward32(self.handle, ptr, batch, _stream_handle(stream)), "ntt_forward32")
+        check(lib().ntt_forward32(self.handle, ptr, batch, _stream_handle(stream, x)), "ntt_forward32")
         return x
 
     def inverse(self, x, stream=None):
         ptr, batch = _dev_ptr(x, self.N, self.L, 32)
-        check(lib().ntt_inverse32(self.handle, ptr, batch, _stream_handle(stream)), "ntt_inverse32")
+        check(lib().ntt_inverse32(self.handle, ptr, batch, _stream_handle(stream, x)), "ntt_inverse32")
         return x
 
     def close(self) -> None:
