@@ -360,3 +360,22 @@ def test_fused_full_size_c4_sampled(form):
         assert np.array_equal(got[b, l], want), (b, l)
     plan.inverse(d)
     assert np.array_equal(to_host(d), x)
+
+
+@pytest.mark.parametrize("logn,batch", [(17, 13), (15, 20), (16, 17), (14, 40)])
+@pytest.mark.parametrize("form", ["2n", "proth"])
+def test_shared_kernel2_ragged_groups(logn, batch, form):
+    """Batches that fill the shared-twiddle Kernel-2's CTAs except the last
+    (2^12 / N2 ciphertexts per CTA): the idle block groups of the last CTA must
+    neither store nor disturb the others."""
+    from paper_2012_01968_b200 import find_primes as lib_find_primes
+    N = 1 << logn
+    primes = lib_find_primes(N, 2, form)
+    psis = [oracle.find_psi(p, N) for p in primes]
+    x = synth.rns_rows(primes, batch, N, config_id=35)
+    plan = Plan(N, primes)
+    d = to_dev(x)
+    plan.forward(d)
+    assert np.array_equal(to_host(d), oracle.ntt_batch(x.copy(), primes, psis, +1))
+    plan.inverse(d)
+    assert np.array_equal(to_host(d), x)
