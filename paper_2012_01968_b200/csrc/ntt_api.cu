@@ -33,9 +33,10 @@ struct ntt_plan_s {
     PrimeConst* d_pc = nullptr;       // [L]
     PrimeConst* d_pc_mont = nullptr;  // [L] the same with N^-1 scaled by 2^64 (NTT-domain products)
     uint64_t table_bytes = 0;
-    // Kernel-1 variant (4 = one tile per CTA, 5 = persistent pipelined); Kernel-2 variant (7 = shared-twiddle
-    // CTA per block position, 5 = persistent pipelined, 6 = pipelined radix 8, 3/4 = one-shot radix 8/16)
-    int loge_k1 = 4, loge_k2 = 7;
+    // Kernel-1 variant (4 = one tile per CTA, 5 = persistent pipelined); Kernel-2 variant (9 = shared-twiddle
+    // CTA per block position on the remainder-last schedule, 7 = the same on the remainder-first schedule,
+    // 5 = persistent pipelined, 6 = pipelined radix 8, 3/4 = one-shot radix 8/16)
+    int loge_k1 = 4, loge_k2 = 9;
     bool proth = false;            // every prime = 1 mod 2^32: PrimeConstP kernels
     bool fused = false;            // single-pass cluster kernel per direction (log_n1 = log2 cluster size)
 };
@@ -332,14 +333,14 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
     p->psis.assign(L, 0);
     // tuning knob (experiments only): NTT_LOGE="k1,k2" per-thread radix exponents
     if (const char* v = std::getenv("NTT_LOGE")) {
-        int a1 = 4, a2 = 7;
-        if (std::sscanf(v, "%d,%d", &a1, &a2) == 2 && (a1 >= 3 && a1 <= 5) && (a2 >= 3 && a2 <= 7)) {
+        int a1 = 4, a2 = 9;
+        if (std::sscanf(v, "%d,%d", &a1, &a2) == 2 && (a1 >= 3 && a1 <= 5) && (a2 >= 3 && a2 <= 9 && a2 != 8)) {
             p->loge_k1 = a1;
             p->loge_k2 = a2;
         }
     }
     // the Proth kernels exist for the default variants only (ntt_kernels.cuh)
-    p->proth = all_proth && (((p->loge_k1 == 4 || p->loge_k1 == 5) && (p->loge_k2 == 5 || p->loge_k2 == 7)) || fused);
+    p->proth = all_proth && (((p->loge_k1 == 4 || p->loge_k1 == 5) && (p->loge_k2 == 5 || p->loge_k2 == 7 || p->loge_k2 == 9)) || fused);
     p->fused = fused;
 
     // host tables, one thread per hardware thread over primes
@@ -397,7 +398,8 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
     const bool k2tab = log_n1 != 0;
     std::vector<Tw> h_fwd2, h_inv2;
     if (k2tab) {
-        const unsigned loge = (!fused && (p->loge_k2 == 3 || p->loge_k2 == 6)) ? 3 : 4;
+        const unsigned loge = (!fused && (p->loge_k2 == 3 || p->loge_k2 == 6)) ? 3
+                              : (!fused && p->loge_k2 == 9) ? (4u | (unsigned)ntt::kRemLast) : 4;
         h_fwd2.resize(N * L);
         h_inv2.resize(N * L);
         std::vector<std::thread> th2;

@@ -295,17 +295,29 @@ __device__ __forceinline__ void static_for(Fn&& f)
 template <int LOGM, int LOGE = 4>
 struct Sched {
     static constexpr int M = 1 << LOGM;
-    static constexpr int LE = LOGM < LOGE ? LOGM : LOGE;
+    // LOGE & 15 is the per-thread radix exponent; LOGE & 16 (kRemLast) puts the
+    // remainder round LAST in forward order instead of first
+    static constexpr bool REMLAST = (LOGE & 16) != 0;
+    static constexpr int LE = LOGM < (LOGE & 15) ? LOGM : (LOGE & 15);
     static constexpr int E = 1 << LE;
-    // A remainder round (LOGM mod LE stages) goes FIRST in forward order: its
-    // stages have the fewest distinct twiddles (one per block for the first
-    // stage), so the many-twiddle last stages run inside full radix-E rounds.
+    // Default: a remainder round (LOGM mod LE stages) goes FIRST in forward
+    // order: its stages have the fewest distinct twiddles (one per block for
+    // the first stage), so the many-twiddle last stages run inside full
+    // radix-E rounds.  REMLAST: full rounds first (round 0 then has stride
+    // M/E and reads global memory in whole segments), remainder last.
     static constexpr int REM = LOGM % LE;
     static constexpr int NR = LOGM / LE + (REM ? 1 : 0);
     static constexpr int TB = M / E;  // threads per sub-transform
-    __host__ __device__ static constexpr int r(int i) { return (REM && i == 0) ? REM : LE; }
-    __host__ __device__ static constexpr int S(int i) { return (REM && i > 0) ? REM + LE * (i - 1) : LE * i; }
+    __host__ __device__ static constexpr int r(int i)
+    {
+        return REMLAST ? ((REM && i == NR - 1) ? REM : LE) : ((REM && i == 0) ? REM : LE);
+    }
+    __host__ __device__ static constexpr int S(int i)
+    {
+        return REMLAST ? LE * i : ((REM && i > 0) ? REM + LE * (i - 1) : LE * i);
+    }
 };
+constexpr int kRemLast = 16;
 
 // Geometry of round RI (stages [S, S+r) of the sub-transform, S = LE RI): the
 // thread's groups are G = qd*TB + tib; group G = (g, o) with
@@ -349,7 +361,10 @@ struct K2Layout {
     __host__ __device__ static constexpr uint32_t used(int OTS)
     {
         if (OTS == 0) return 1u << LOGM;
-        const int Sl = SC::S(SC::NR - 1), i0 = LOGM - OTS - Sl;
+        const int j0 = LOGM - OTS;  // first OT stage; its round and position in it
+        int ri = SC::NR - 1;
+        while (SC::S(ri) > j0) --ri;
+        const int Sl = SC::S(ri), i0 = j0 - Sl;
         return round_off(Sl) + (((1u << i0) - 1u) << Sl);
     }
 };

@@ -510,10 +510,10 @@ struct SharedCfg {
     static constexpr int MINB = INV ? 4 : 3;
 };
 
-template <int LOGM, bool INV, int OTS, bool MUL = false, class PCT = PrimeConst>
+template <int LOGM, bool INV, int OTS, bool MUL = false, class PCT = PrimeConst, int LE2 = 4>
 __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>::MINB) k_shared(const KArgs a)
 {
-    using SC = Sched<LOGM, 4>;
+    using SC = Sched<LOGM, LE2>;
     using CC = SharedCfg<LOGM, INV>;
     constexpr int M = SC::M, E = SC::E, TB = SC::TB, NR = SC::NR, NB = CC::NB, CT = CC::CT;
     constexpr int OT_FROM = OTS ? LOGM - OTS : (1 << 20);
@@ -535,13 +535,13 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
 
     {  // the block position's twiddle segment, once per CTA (under OT only the prefix of the table stages)
         const Tw* t2 = a.tab2 + ((uint64_t)l << a.logn) + ((uint64_t)bb << LOGM);
-        constexpr uint32_t USED = K2Layout<LOGM, 4>::used(OTS);
+        constexpr uint32_t USED = K2Layout<LOGM, LE2>::used(OTS);
         for (uint32_t i = tid; i < USED; i += CT) cp_async16(tws + i, t2 + i);
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
     uint64_t* sb = sm + blk * M;
     auto tabf = [&](const TwKey& k) {
-        return tws[K2Layout<LOGM, 4>::round_off(k.S) + ((((1u << k.i) - 1u + k.h) << k.S) + k.g)];
+        return tws[K2Layout<LOGM, LE2>::round_off(k.S) + ((((1u << k.i) - 1u + k.h) << k.S) + k.g)];
     };
     auto otf = [&](uint32_t idx) {
         const uint32_t e = __brev(idx) >> (32 - a.logn);  // exponent of Psi[idx]
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
     uint64_t x[16];
     // element (qd, k) of the round at swz_at<elem(qd TB, k)>(swz(elem(tib, 0)))
     auto s_load = [&](auto ri) {
-        using Geo = RoundGeo<LOGM, decltype(ri)::value, 4>;
+        using Geo = RoundGeo<LOGM, decltype(ri)::value, LE2>;
         const uint32_t sB = swz(Geo::elem(tib, 0));
         static_for<Geo::GPT>([&](auto qdc) {
             constexpr int qd = decltype(qdc)::value;
@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
         });
     };
     auto s_store = [&](auto ri) {
-        using Geo = RoundGeo<LOGM, decltype(ri)::value, 4>;
+        using Geo = RoundGeo<LOGM, decltype(ri)::value, LE2>;
         const uint32_t sB = swz(Geo::elem(tib, 0));
         static_for<Geo::GPT>([&](auto qdc) {
             constexpr int qd = decltype(qdc)::value;
@@ -589,8 +589,11 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
             }
         });
     };
-    constexpr bool DIRECT0 = RoundGeo<LOGM, 0, 4>::s >= 16;
+    constexpr bool DIRECT0 = RoundGeo<LOGM, 0, LE2>::s >= 16;
     static_assert(DIRECT0, "round 0 is read / written straight from global");
+    // remainder-last schedule with a single-stage remainder: the last forward
+    // round is radix-2 on adjacent pairs, read / written straight from global
+    constexpr bool DIRECT_LAST = SC::REMLAST && SC::REM == 1;
     auto twiddles_ready = [&]() {
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
@@ -598,7 +601,7 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
 
     if constexpr (!INV) {
         {  // round 0 straight from global: whole 128-byte segments per warp
-            using Geo = RoundGeo<LOGM, 0, 4>;
+            using Geo = RoundGeo<LOGM, 0, LE2>;
 #pragma unroll
             for (int qd = 0; qd < Geo::GPT; ++qd)
 #pragma unroll
@@ -608,15 +611,27 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
         static_for<NR>([&](auto ri) {
             constexpr int RI = decltype(ri)::value;
             if constexpr (RI > 0) s_load(ri);
-            ct_round<LOGM, 4, RI, OT_FROM, false, true>(x, tib, Fm1, tabf, otf, pc);
+            ct_round<LOGM, LE2, RI, OT_FROM, false, true>(x, tib, Fm1, tabf, otf, pc);
             if constexpr (RI == NR - 1) {
 #pragma unroll
                 for (int k = 0; k < E; ++k) x[k] = norm8(x[k], pc);  // any word (lazy < 16p + 2^32) -> [0,p)
             }
-            s_store(ri);
-            block_sync<TB>(blk);
+            if constexpr (DIRECT_LAST && RI == NR - 1) {
+                // remainder-last radix-2 round: the thread's pairs (2G, 2G+1) go
+                // straight to global, lanes contiguous (512 bytes per warp store)
+                using Geo = RoundGeo<LOGM, RI, LE2>;
+                if (active) {
+#pragma unroll
+                    for (int qd = 0; qd < Geo::GPT; ++qd)
+                        *reinterpret_cast<ulonglong2*>(g + Geo::elem(qd * TB + tib, 0)) =
+                            make_ulonglong2(x[2 * qd], x[2 * qd + 1]);
+                }
+            } else {
+                s_store(ri);
+                block_sync<TB>(blk);
+            }
         });
-        if (active) {  // 128-bit coalesced stores; word 2 ch = 2 j TB + 2 tib
+        if (!DIRECT_LAST && active) {  // 128-bit coalesced stores; word 2 ch = 2 j TB + 2 tib
             const uint32_t s2 = swz(2 * tib);
             static_for<E / 2>([&](auto jc) {
                 constexpr int j = decltype(jc)::value;
@@ -624,7 +639,7 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
                     *reinterpret_cast<const ulonglong2*>(sb + swz_at<2 * j * TB>(s2));
             });
         }
-    } else {
+    } else if constexpr (!DIRECT_LAST) {
         const uint32_t s2 = swz(2 * tib);
         static_for<E / 2>([&](auto jc) {
             constexpr int j = decltype(jc)::value;
@@ -642,14 +657,51 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
             constexpr int RI = NR - 1 - decltype(rj)::value;
             using RC = std::integral_constant<int, RI>;
             s_load(RC{});
-            gs_round<LOGM, 4, RI, OT_FROM, false>(x, tib, Fm1, tabf, otf, pc);
+            gs_round<LOGM, LE2, RI, OT_FROM, false>(x, tib, Fm1, tabf, otf, pc);
             if constexpr (RI > 0) {
                 s_store(RC{});
                 block_sync<TB>(blk);
             }
         });
         if (active) {  // round 0 straight to global
-            using Geo = RoundGeo<LOGM, 0, 4>;
+            using Geo = RoundGeo<LOGM, 0, LE2>;
+#pragma unroll
+            for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+                for (int k = 0; k < Geo::R; ++k) g[Geo::elem(qd * TB + tib, k)] = x[qd * Geo::R + k];
+        }
+    } else {
+        // remainder-last: the first inverse round (the radix-2 remainder) reads
+        // its pairs (2G, 2G+1) straight from global -- no SMEM staging
+        static_for<NR>([&](auto rj) {
+            constexpr int RI = NR - 1 - decltype(rj)::value;
+            using RC = std::integral_constant<int, RI>;
+            if constexpr (RI == NR - 1) {
+                using Geo = RoundGeo<LOGM, RI, LE2>;
+#pragma unroll
+                for (int qd = 0; qd < Geo::GPT; ++qd) {
+                    const uint32_t e = Geo::elem(qd * TB + tib, 0);
+                    ulonglong2 v = *reinterpret_cast<const ulonglong2*>(g + e);
+                    if constexpr (MUL) {  // fused NTT-domain product (ntt_pointwise_inverse)
+                        const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(a.mul_a + (g - a.data) + e);
+                        v.x = mont_mul(u.x, v.x, pc);
+                        v.y = mont_mul(u.y, v.y, pc);
+                    }
+                    x[2 * qd] = v.x;
+                    x[2 * qd + 1] = v.y;
+                }
+                twiddles_ready();
+            } else {
+                s_load(RC{});
+            }
+            gs_round<LOGM, LE2, RI, OT_FROM, false>(x, tib, Fm1, tabf, otf, pc);
+            if constexpr (RI > 0) {
+                s_store(RC{});
+                block_sync<TB>(blk);
+            }
+        });
+        if (active) {  // round 0 straight to global
+            using Geo = RoundGeo<LOGM, 0, LE2>;
 #pragma unroll
             for (int qd = 0; qd < Geo::GPT; ++qd)
 #pragma unroll
@@ -918,11 +970,11 @@ cudaError_t launch_blocks_t(KArgs a, cudaStream_t st)
     return cudaPeekAtLastError();
 }
 
-template <int LOGM, bool INV, int OTS, bool MUL, class PCT>
+template <int LOGM, bool INV, int OTS, bool MUL, class PCT, int LE2>
 cudaError_t launch_shared_t(const KArgs& a, cudaStream_t st)
 {
     using CC = SharedCfg<LOGM, INV>;
-    auto fn = k_shared<LOGM, INV, OTS, MUL, PCT>;
+    auto fn = k_shared<LOGM, INV, OTS, MUL, PCT, LE2>;
     static std::atomic<uint64_t> attr_set{0};  // one bit per device
     if (!set_once(attr_set)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
     const uint64_t grid = ((uint64_t)a.L << a.log_n1) * ((a.batch + CC::NB - 1) / CC::NB);
@@ -930,31 +982,45 @@ cudaError_t launch_shared_t(const KArgs& a, cudaStream_t st)
     return cudaPeekAtLastError();
 }
 
+template <int LOGM, bool INV, class PCT, int LE2>
+cudaError_t launch_shared_ot2(const KArgs& a, int ots, cudaStream_t st)
+{
+    if (a.mul_a) {
+        if constexpr (INV) {
+            if (ots == 0) return launch_shared_t<LOGM, INV, 0, true, PCT, LE2>(a, st);
+        }
+        return cudaErrorNotSupported;
+    }
+    switch (ots) {
+        case 0: return launch_shared_t<LOGM, INV, 0, false, PCT, LE2>(a, st);
+        case 1: return launch_shared_t<LOGM, INV, 1, false, PCT, LE2>(a, st);
+        default: return launch_shared_t<LOGM, INV, 2, false, PCT, LE2>(a, st);
+    }
+}
+
+// remlast: the remainder-last schedule (tuning knob 9; the plan's Kernel-2
+// table is built for it)
 template <int LOGM, bool INV, class PCT>
-cudaError_t launch_shared_ot(const KArgs& a, int ots, cudaStream_t st)
+cudaError_t launch_shared_ot(const KArgs& a, int ots, bool remlast, cudaStream_t st)
 {
     if constexpr (RoundGeo<LOGM, 0, 4>::s < 16) {
         return cudaErrorNotSupported;
     } else {
-        if (a.mul_a) {
-            if constexpr (INV) {
-                if (ots == 0) return launch_shared_t<LOGM, INV, 0, true, PCT>(a, st);
-            }
+        if (remlast) {
+            if constexpr (RoundGeo<LOGM, 0, 4 | kRemLast>::s >= 16)
+                return launch_shared_ot2<LOGM, INV, PCT, 4 | kRemLast>(a, ots, st);
             return cudaErrorNotSupported;
         }
-        switch (ots) {
-            case 0: return launch_shared_t<LOGM, INV, 0, false, PCT>(a, st);
-            case 1: return launch_shared_t<LOGM, INV, 1, false, PCT>(a, st);
-            default: return launch_shared_t<LOGM, INV, 2, false, PCT>(a, st);
-        }
+        return launch_shared_ot2<LOGM, INV, PCT, 4>(a, ots, st);
     }
 }
 
 template <bool INV, class PCT, int... Ls>
-cudaError_t shared_switch(int logm, const KArgs& a, int ots, cudaStream_t st, std::integer_sequence<int, Ls...>)
+cudaError_t shared_switch(int logm, const KArgs& a, int ots, bool remlast, cudaStream_t st,
+                          std::integer_sequence<int, Ls...>)
 {
     cudaError_t err = cudaErrorInvalidValue;
-    ((logm == Ls ? (err = launch_shared_ot<Ls, INV, PCT>(a, ots, st), 0) : 0), ...);
+    ((logm == Ls ? (err = launch_shared_ot<Ls, INV, PCT>(a, ots, remlast, st), 0) : 0), ...);
     return err;
 }
 
@@ -1075,9 +1141,15 @@ cudaError_t launch_k2_t(bool inverse, int loge, const KArgs& a, int ots, uint32_
     // ciphertexts) when the batch fills its CTAs (NB = 2^12 / N2 ciphertexts);
     // smaller batches (e.g. the C5 request stream, batch 1) take the persistent
     // pipelined Kernel-2, whose warps walk blocks of any row
-    if (loge == 7 && a.batch >= (4096u >> logm))
-        return inverse ? shared_switch<true, PCT>(logm, a, ots, st, K2Sizes{})
-                       : shared_switch<false, PCT>(logm, a, ots, st, K2Sizes{});
+    // (knob 9: the same kernel on the remainder-last schedule)
+    // (the remainder-last schedule reads round 0 from global at stride N2/16,
+    // whole segments only for N2 >= 2^8; smaller blocks take the persistent kernel)
+    if ((loge == 7 || (loge == 9 && logm >= 8)) && a.batch >= (4096u >> logm))
+        return inverse ? shared_switch<true, PCT>(logm, a, ots, loge == 9, st, K2Sizes{})
+                       : shared_switch<false, PCT>(logm, a, ots, loge == 9, st, K2Sizes{});
+    if (loge == 9)  // remainder-last table: the persistent Kernel-2 on the same schedule
+        return inverse ? blocks_switch<4 | kRemLast, true, PCT>(logm, a, ots, st, K2Sizes{})
+                       : blocks_switch<4 | kRemLast, false, PCT>(logm, a, ots, st, K2Sizes{});
     if (loge == 7) loge = 5;
     if (loge == 5)  // pipelined persistent Kernel-2 (radix 16)
         return inverse ? blocks_switch<4, true, PCT>(logm, a, ots, st, K2Sizes{})

@@ -41,7 +41,9 @@ Twiddle32 shoup_pair32(uint32_t w, uint32_t p);
 template <class T>
 void k2_order(const T* std_tab, unsigned logn, unsigned log_n1, unsigned loge, T* out)
 {
-    const unsigned logm = logn - log_n1, le = loge < logm ? loge : logm;
+    // loge & 15: radix exponent; loge & 16: remainder round last (ntt::Sched)
+    const bool remlast = (loge & 16u) != 0;
+    const unsigned logm = logn - log_n1, le = (loge & 15u) < logm ? (loge & 15u) : logm;
     const uint32_t N1 = 1u << log_n1, N2 = 1u << logm;
     for (uint32_t bb = 0; bb < N1; ++bb) {
         const uint32_t F = N1 + bb;
@@ -50,7 +52,7 @@ void k2_order(const T* std_tab, unsigned logn, unsigned log_n1, unsigned loge, T
         uint32_t off = 1;
         const unsigned rem = logm % le;
         for (unsigned S = 0; S < logm;) {
-            const unsigned r = (S == 0 && rem) ? rem : le;
+            const unsigned r = remlast ? (logm - S < le ? logm - S : le) : ((S == 0 && rem) ? rem : le);
             for (unsigned i = 0; i < r; ++i)
                 for (uint32_t h = 0; h < (1u << i); ++h)
                     for (uint32_t g = 0; g < (1u << S); ++g)

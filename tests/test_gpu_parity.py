@@ -287,7 +287,7 @@ def test_c5_prime_sweep(L):
     check_roundtrip(1 << 16, L, 1)
 
 
-@pytest.mark.parametrize("variant", ["4,3", "4,4", "4,5", "4,6", "4,7", "5,5"])
+@pytest.mark.parametrize("variant", ["4,3", "4,4", "4,5", "4,6", "4,7", "4,9", "5,5"])
 @pytest.mark.parametrize("logn,log_n1", [(14, 7), (15, 7), (16, 8), (17, 8), (17, 7), (17, 9)])
 def test_kernel2_variants(variant, logn, log_n1, monkeypatch):
     """Kernel-2 implementations (radix 8 / 16, one-shot / pipelined persistent)

@@ -139,7 +139,7 @@ def test_proth_full_size_c4():
     assert np.array_equal(to_host(d), x)
 
 
-@pytest.mark.parametrize("variant", ["4,5", "4,7", "5,7"])
+@pytest.mark.parametrize("variant", ["4,5", "4,7", "4,9", "5,7"])
 @pytest.mark.parametrize("logn,log_n1", [(14, 7), (16, 8), (17, 8), (17, 6), (17, 9)])
 def test_proth_kernel_variants(variant, logn, log_n1, monkeypatch):
     """Kernel variants with Proth instantiations (NTT_LOGE knob), OT on and off."""
