@@ -237,11 +237,11 @@ struct Contig32Cfg {
 #ifndef NTT32_K2_MINB
 #define NTT32_K2_MINB 4  // 64 registers, 4 CTAs / 32 warps per SM (measured 2 % faster than 2)
 #endif
-template <int LOGM, bool INV, bool FUSE0, bool K2, bool SHARED = false>
+template <int LOGM, bool INV, bool FUSE0, bool K2, bool SHARED = false, int LE2 = 4>
 __global__ void __launch_bounds__(Contig32Cfg<LOGM>::CT,
                                   Contig32Cfg<LOGM>::CT > 256 ? 1 : (K2 ? NTT32_K2_MINB : 2)) k32_contig(const KArgs32 a)
 {
-    using SC = Sched<LOGM, 4>;
+    using SC = Sched<LOGM, LE2>;
     constexpr int M = SC::M, E = SC::E, TB = SC::TB, NR = SC::NR, NB = Contig32Cfg<LOGM>::NB;
     extern __shared__ __align__(16) uint32_t sm32[];
     const uint32_t tid = threadIdx.x, blk = tid / TB, tib = tid % TB;
@@ -276,14 +276,23 @@ __global__ void __launch_bounds__(Contig32Cfg<LOGM>::CT,
     }
     auto tabf = [&](const TwKey& k) {
         if constexpr (SHARED)
-            return tws[K2Layout<LOGM, 4>::round_off(k.S) + ((((1u << k.i) - 1u + k.h) << k.S) + k.g)];
+            return tws[K2Layout<LOGM, LE2>::round_off(k.S) + ((((1u << k.i) - 1u + k.h) << k.S) + k.g)];
         else if constexpr (K2)
-            return ldg_tw(tb2 + K2Layout<LOGM, 4>::round_off(k.S) + ((((1u << k.i) - 1u + k.h) << k.S) + k.g));
+            return ldg_tw(tb2 + K2Layout<LOGM, LE2>::round_off(k.S) + ((((1u << k.i) - 1u + k.h) << k.S) + k.g));
         else
             return ldg_tw(tab + k.idx);
     };
 
-    // global -> SMEM (E/4 16-byte chunks per thread)
+    // SHARED on the remainder-last schedule: the forward reads round 0 (stride
+    // >= 8 words) and the inverse writes it straight from/to global; with a
+    // single-stage remainder the last forward round (adjacent pairs) is also
+    // stored, and the first inverse round loaded, straight to/from global
+    constexpr bool DIRECT = SHARED && SC::REMLAST;
+    constexpr bool DIRECT_LAST = DIRECT && SC::REM == 1;
+    // global -> SMEM (E/4 16-byte chunks per thread), unless the first round
+    // reads global itself (forward: round 0; inverse: the pair round)
+    constexpr bool STAGED_IN = INV ? !DIRECT_LAST : !DIRECT;
+    if constexpr (STAGED_IN)
 #pragma unroll
     for (int j = 0; j < (E >= 4 ? E / 4 : 1); ++j) {
         const uint32_t ch = j * TB + tib;
@@ -299,7 +308,7 @@ __global__ void __launch_bounds__(Contig32Cfg<LOGM>::CT,
     uint32_t x[16];
     // element (qd, k) at swz32_at<elem(qd TB, k)>(swz32(elem(tib, 0))): one base per round
     auto s_io = [&](auto ri, bool store) {
-        using Geo = RoundGeo<LOGM, decltype(ri)::value, 4>;
+        using Geo = RoundGeo<LOGM, decltype(ri)::value, LE2>;
         const uint32_t sB = swz32(Geo::elem(tib, 0));
         static_for<Geo::GPT>([&](auto qdc) {
             constexpr int qd = decltype(qdc)::value;
@@ -313,32 +322,79 @@ __global__ void __launch_bounds__(Contig32Cfg<LOGM>::CT,
             });
         });
     };
+    auto g_io0 = [&](bool store) {  // round 0 straight from / to global
+        using Geo = RoundGeo<LOGM, 0, LE2>;
+#pragma unroll
+        for (int qd = 0; qd < Geo::GPT; ++qd)
+#pragma unroll
+            for (int k = 0; k < Geo::R; ++k) {
+                const uint32_t e = Geo::elem(qd * TB + tib, k);
+                if (store)
+                    g[e] = x[qd * Geo::R + k];
+                else
+                    x[qd * Geo::R + k] = g[e];
+            }
+    };
+    auto g_pairs = [&](bool store) {  // the remainder-last radix-2 round's pairs (2G, 2G+1)
+        using Geo = RoundGeo<LOGM, NR - 1, LE2>;
+#pragma unroll
+        for (int qd = 0; qd < Geo::GPT; ++qd) {
+            uint2* p = reinterpret_cast<uint2*>(g + Geo::elem(qd * TB + tib, 0));
+            if (store) {
+                *p = make_uint2(x[2 * qd], x[2 * qd + 1]);
+            } else {
+                const uint2 v = *p;
+                x[2 * qd] = v.x;
+                x[2 * qd + 1] = v.y;
+            }
+        }
+    };
     if constexpr (!INV) {
         static_for<NR>([&](auto ri) {
             constexpr int RI = decltype(ri)::value;
-            s_io(ri, false);
-            ct_round<LOGM, 4, RI>(x, tib, tabf, pc);
+            if constexpr (DIRECT && RI == 0) {
+                g_io0(false);
+                __syncthreads();  // the twiddle segment is in SMEM
+            } else {
+                s_io(ri, false);
+            }
+            ct_round<LOGM, LE2, RI>(x, tib, tabf, pc);
             if constexpr (RI == NR - 1) {
 #pragma unroll
                 for (int k = 0; k < E; ++k) x[k] = csub(csub(x[k], pc.p2), pc.p);
             }
-            s_io(ri, true);
-            __syncthreads();
+            if constexpr (DIRECT_LAST && RI == NR - 1) {
+                if (active) g_pairs(true);
+            } else {
+                s_io(ri, true);
+                __syncthreads();
+            }
         });
     } else {
         static_for<NR>([&](auto rj) {
             constexpr int RI = NR - 1 - decltype(rj)::value;
             using RC = std::integral_constant<int, RI>;
-            s_io(RC{}, false);
-            gs_round<LOGM, 4, RI, FUSE0>(x, tib, tabf, pc);
+            if constexpr (DIRECT_LAST && RI == NR - 1) {
+                g_pairs(false);
+                __syncthreads();  // the twiddle segment is in SMEM
+            } else {
+                s_io(RC{}, false);
+            }
+            gs_round<LOGM, LE2, RI, FUSE0>(x, tib, tabf, pc);
             if constexpr (FUSE0 && RI == 0) {
 #pragma unroll
                 for (int k = 0; k < E; ++k) x[k] = csub(x[k], pc.p);
             }
-            s_io(RC{}, true);
-            __syncthreads();
+            if constexpr (DIRECT && RI == 0) {
+                if (active) g_io0(true);
+            } else {
+                s_io(RC{}, true);
+                __syncthreads();
+            }
         });
     }
+    constexpr bool STAGED_OUT = INV ? !DIRECT : !DIRECT_LAST;
+    if constexpr (STAGED_OUT)
     if (active) {
 #pragma unroll
         for (int j = 0; j < (E >= 4 ? E / 4 : 1); ++j) {
@@ -381,7 +437,8 @@ cudaError_t launch32_contig_t(const KArgs32& a, cudaStream_t st)
 {
     using CC = w32::Contig32Cfg<LOGM>;
     const size_t smem = (size_t)CC::NB * (1 << LOGM) * 4 + (SHARED ? sizeof(Tw32) << LOGM : 0);
-    auto fn = w32::k32_contig<LOGM, INV, FUSE0, K2, SHARED>;
+    // Kernel-2 runs the remainder-last schedule (the plan's Kernel-2 table follows it)
+    auto fn = w32::k32_contig<LOGM, INV, FUSE0, K2, SHARED, K2 ? (4 | kRemLast) : 4>;
     static std::atomic<uint64_t> attr{0};
     if (!set_once32(attr)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const uint32_t grid = SHARED ? (a.L << a.log_n1) * ((a.batch + CC::NB - 1) / CC::NB)

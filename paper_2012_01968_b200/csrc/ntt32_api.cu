@@ -158,7 +158,9 @@ ntt_status_t ntt_plan_create32(ntt32_plan_t* out, unsigned n, const uint32_t* pr
                         const nttp::Twiddle32 t32 = nttp::shoup_pair32((uint32_t)wide[i].w, q);
                         tab[i] = Tw32{t32.w, t32.wb};
                     }
-                    if (l1) nttp::k2_order(tab, logn, l1, 4, (dir ? h_inv2.data() : h_fwd2.data()) + l * N);
+                    if (l1)  // remainder-last round order, as the 32-bit Kernel-2 runs it
+                        nttp::k2_order(tab, logn, l1, 4u | (unsigned)ntt::kRemLast,
+                                       (dir ? h_inv2.data() : h_fwd2.data()) + l * N);
                 }
                 const uint32_t ninv = (uint32_t)nttp::pow_mod(N % q, q - 2, q);
                 const uint32_t ninv_psi = (uint32_t)nttp::mul_mod(ninv, h_inv[l * N + (N > 1 ? 1 : 0)].w, q);

@@ -379,3 +379,8 @@ def test_shared_kernel2_ragged_groups(logn, batch, form):
     assert np.array_equal(to_host(d), oracle.ntt_batch(x.copy(), primes, psis, +1))
     plan.inverse(d)
     assert np.array_equal(to_host(d), x)
+    # the inverse alone on fresh NTT-domain words (no state left from the forward)
+    y = synth.rns_rows(primes, batch, N, config_id=36)
+    d = to_dev(y)
+    plan.inverse(d)
+    assert np.array_equal(to_host(d), oracle.ntt_batch(y.copy(), primes, psis, -1))

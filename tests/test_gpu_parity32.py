@@ -115,3 +115,13 @@ def test_errors_32():
         plan.forward(t[1:])  # 4-byte offset: misaligned
     assert e.value.status == -4
     plan.close()
+
+
+@pytest.mark.parametrize("logn,batch", [(17, 8), (17, 11), (16, 16), (16, 21), (15, 16), (14, 32), (14, 35)])
+def test_shared_kernel2_32(logn, batch):
+    """Batches that fill the 32-bit shared-twiddle Kernel-2 (2^12 / N2
+    ciphertexts per CTA), including a ragged last group: forward against the
+    oracle on every row, exact round trip -- the remainder-last schedule with
+    its direct global ends (single-stage remainder at N2 = 2^9) and without."""
+    N = 1 << logn
+    check32(N, 2, batch, config_id=40)
