@@ -4,5 +4,5 @@
 mkdir -p gpurun_out/ab
 for v in "$@"; do
   cp tools/libs/libntt_$v.so paper_2012_01968_b200/libntt.so
-  echo "== $v"; python tools/variants.py --variants "4,7" --primes proth
+  echo "== $v"; python tools/variants.py --variants "${AB_VARIANTS:-4,9}" --primes proth
 done > gpurun_out/ab/ab.jsonl 2>&1
