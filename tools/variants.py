@@ -26,7 +26,7 @@ ap.add_argument("--config", default="C4")
 ap.add_argument("--steps", type=int, default=10)
 ap.add_argument("--ot", action="store_true")
 ap.add_argument("--log-n1", type=int, default=0)
-ap.add_argument("--variants", default="4,4;3,3;4,3;3,4")
+ap.add_argument("--variants", default="4,9;4,7;4,5")
 ap.add_argument("--primes", default="proth", choices=["2n", "proth"])
 a = ap.parse_args()
 logn, L, B, _ = CONFIGS[a.config]
