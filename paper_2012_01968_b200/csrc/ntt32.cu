@@ -25,6 +25,18 @@ __device__ __forceinline__ uint32_t shoup(uint32_t b, uint32_t w, uint32_t wb, u
 }
 __device__ __forceinline__ uint32_t csub(uint32_t x, uint32_t m) { return x >= m ? x - m : x; }
 
+// Barrier over the TB threads of one block (__syncwarp when a warp holds whole
+// blocks, else a named barrier of the block's own)
+template <int TB>
+__device__ __forceinline__ void bsync(uint32_t blk)
+{
+    if constexpr (TB <= 32) {
+        __syncwarp();
+    } else {
+        asm volatile("bar.sync %0, %1;" ::"r"(blk + 1), "n"(TB) : "memory");
+    }
+}
+
 struct Mul {
     Tw32 t;
     __device__ __forceinline__ uint32_t mul(uint32_t x, const PrimeConst32& c) const { return shoup(x, t.w, t.wb, c.p); }
@@ -367,7 +379,7 @@ __global__ void __launch_bounds__(Contig32Cfg<LOGM>::CT,
                 if (active) g_pairs(true);
             } else {
                 s_io(ri, true);
-                __syncthreads();
+                bsync<TB>(blk);  // blocks never share SMEM: block-local barrier
             }
         });
     } else {
@@ -389,7 +401,7 @@ __global__ void __launch_bounds__(Contig32Cfg<LOGM>::CT,
                 if (active) g_io0(true);
             } else {
                 s_io(RC{}, true);
-                __syncthreads();
+                bsync<TB>(blk);  // blocks never share SMEM: block-local barrier
             }
         });
     }
