@@ -1,25 +1,38 @@
 #!/usr/bin/env python3
 """bench.py -- the headline measurement of the batched negacyclic NTT + iNTT.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--scaling strong|weak]
+                    [--primes 2n|proth] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (python bench.py --gpus N re-launches itself so)
 
 A "step" is one pass of the whole hot path over one batch: ntt_forward then
 ntt_inverse of every residue row.  Workload at N=1:
-BASELINE.json configs[3] ("C4": N=2^17, 60 primes of 60 bits, batch 32).
-Multi-GPU is weak-scaled and prime-sharded: G ranks process 32*G ciphertexts,
-split over a Gp x Gb grid of (prime range, ciphertext range) shards so every
-rank holds exactly 1920 rows; there is no collective on the data path
-(SURVEY 8(e)); NCCL carries only the timing barrier / max.
+BASELINE.json configs[3] ("C4": N=2^17, 60 primes of 60 bits, batch 32),
+primes = the R3 chain (p = 1 mod 2N scanned down from 2^60 - 2N + 1, SURVEY
+8(c)#3); the Proth chain is reported beside it at equal rank ("proth").
 
-Prints ONE JSON line on rank 0 (see DESIGN.md section 7 for every key).
+Multi-GPU: the rows are independent, so the job shards with no
+data-path collective.  --scaling strong (default): the fixed C4 job (32
+ciphertexts x 60 primes) is split into contiguous prime ranges, one per rank
+(30/30, 15x4, 8/8/8/8/7/7/7/7).  --scaling weak: 32 ciphertexts per GPU.
+NCCL (torch.distributed) carries the barriers, the max-over-ranks time and,
+after timing, the per-row checksums that rank 0 checks against the oracle.
+
+--config C5 (mixed request stream, N=2^16, L swept over 1..45): throughput
+mode (whole requests round-robin to ranks, batched per L) and latency mode
+(one request at a time, its primes sharded over the ranks, replayed from a
+request graph), microseconds per request for each L.
+
+Prints ONE JSON line on rank 0 (DESIGN.md section 7 explains every key).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -32,21 +45,27 @@ sys.path.insert(0, ROOT)
 METRIC = "µs per NTT+iNTT (N=2^17, all primes) & HBM GB/s vs 8 TB/s, 1/2/4/8 B200"
 
 CONFIGS = {
-    # name: (logN, L, batch per GPU, BASELINE.json text)
+    # name: (logN, L, batch of the job, BASELINE.json text)
     "C1": (12, 1, 1, "N=2^12, 1 prime (~60-bit), batch 1"),
     "C2": (15, 15, 16, "N=2^15, 15 primes (~Q=2^881, SEAL-like), batch 16"),
     "C3": (16, 45, 64, "N=2^16, 45 primes (bootstrappable CKKS-size), batch 64"),
     "C4": (17, 60, 32, "N=2^17, ~60 primes (large bootstrappable set), batch 32"),
+    "C5": (16, 45, 64, "mixed ciphertext stream: N=2^16, L sweep 1-45 primes, latency vs throughput"),
 }
+C5_LS = [1, 2, 4, 8, 15, 30, 45]
+C5_REQUESTS = 64  # requests per L in throughput mode
+PRIME_TEXT = {"2n": "p = 1 mod 2N descending from 2^60 - 2N + 1 (SURVEY 8(c)#3, DESIGN.md R3)",
+              "proth": "p = 1 mod 2^32 descending from 2^60 - 2^32 + 1 (DESIGN.md R18)"}
+L2_BYTES = 126 * 2**20
 
 
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 # Multiply-pipe cost of one warp-instruction per SMSP, in clocks: IMAD from the
@@ -54,24 +73,38 @@ def peaks():
 # chains (profiles/r01_alu_roof.jsonl: 24 and 28 per clk per SM; confirmed by
 # the 2 WIDE + 2 HI + 3 IMAD mix at 25.7 clk, profiles/r01g_bf_roof_variants.txt).
 CLK_IMAD, CLK_WIDE, CLK_HI = 2.0, 16 / 3.0, 32 / 7.0
+SM_COUNT, SM_GHZ = 148, 1.965
 
 
-def alu_floor_clk(form: str = "2n") -> float:
-    """Multiply-pipe clocks per warp-butterfly of the truncated-quotient Shoup
-    butterfly: general primes 3 WIDE + 2 HI + 4 IMAD, Proth
+def alu_floor_clk(form: str) -> float:
+    """Multiply-pipe clocks per warp-modmul of the truncated-quotient Shoup
+    multiply: general primes 3 WIDE + 2 HI + 4 IMAD, Proth
     primes 2 WIDE + 2 HI + 3 IMAD."""
     if form == "proth":
         return 2 * CLK_WIDE + 2 * CLK_HI + 3 * CLK_IMAD
     return 3 * CLK_WIDE + 2 * CLK_HI + 4 * CLK_IMAD
 
 
-def alu_peak(form: str = "2n", nominal: bool = False):
-    """Derived integer roof in G butterflies/s: 148 SMs x 4 SMSPs x 32 lanes /
-    (clk per warp-butterfly) x 1.965 GHz.  nominal=True uses quarter-rate
-    (4 clk) WIDE/HI instead of the measured rates (an upper bound)."""
-    sm_clk_ghz = 1.965
-    clk = (22.0 if form == "proth" else 28.0) if nominal else alu_floor_clk(form)
-    return 148 * 4 * 32 / clk * sm_clk_ghz
+def alu_peak(form: str) -> float:
+    """Derived integer roof in G modmul/s: 148 SMs x 4 SMSPs x 32 lanes /
+    (multiply-pipe clk per warp-modmul) x 1.965 GHz."""
+    return SM_COUNT * 4 * 32 / alu_floor_clk(form) * SM_GHZ
+
+
+def butterfly_ceiling():
+    """The practical ceiling, measured live: tools/libs/bf_roof runs the
+    kernels' own CT / GS butterflies (radix-16 rounds on registers, twiddles
+    broadcast from SMEM, 32 warps/SM, no memory).  {"ct_2n": G/s, ...}."""
+    exe = os.path.join(ROOT, "tools", "libs", "bf_roof")
+    out = {}
+    try:
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+        for line in r.stdout.splitlines():
+            d = json.loads(line)
+            out[f"{d['butterfly']}_{d['primes']}"] = d["Gbutterfly_s"]
+    except Exception as e:  # reported, not hidden
+        out["error"] = repr(e)
+    return out
 
 
 # ------------------------------------------------------------------ clocks
@@ -129,15 +162,36 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-# ------------------------------------------------------------------ sharding
+# ------------------------------------------------------------------ sharding (SURVEY 8(e))
+
+def prime_ranges(G: int, L: int) -> list[tuple[int, int]]:
+    """Contiguous prime ranges (offset, count) of L primes over G ranks, the
+    first L mod G ranks one prime larger: 60 over 8 -> 8,8,8,8,7,7,7,7."""
+    base, extra = divmod(L, G)
+    out, off = [], 0
+    for r in range(G):
+        n = base + (1 if r < extra else 0)
+        out.append((off, n))
+        off += n
+    return out
+
+
+def strong_shard(rank: int, G: int, L: int, batch: int) -> dict:
+    """Strong scaling: the fixed job (batch ciphertexts x L primes) split into
+    contiguous prime ranges; every rank holds all ciphertexts of its primes."""
+    off, n = prime_ranges(G, L)[rank]
+    return {"prime_offset": off, "L": n, "batch_offset": 0, "batch": batch, "Gp": G, "Gb": 1}
+
 
 def shard_grid(G: int, L: int):
-    """(Gp, Gb): the largest Gp <= G dividing both G and L, Gb = G / Gp."""
+    """(Gp, Gb) for weak scaling: the largest Gp <= G dividing both G and L, Gb = G / Gp."""
     gp = max(d for d in range(1, G + 1) if G % d == 0 and L % d == 0)
     return gp, G // gp
 
 
-def my_shard(rank: int, G: int, L: int, batch_per_gpu: int):
+def weak_shard(rank: int, G: int, L: int, batch_per_gpu: int) -> dict:
+    """Weak scaling: batch_per_gpu * G ciphertexts over a Gp x Gb grid of
+    (prime range, ciphertext range) shards, every rank batch_per_gpu * L rows."""
     gp, gb = shard_grid(G, L)
     rp, rb = rank % gp, rank // gp
     Lp = L // gp
@@ -145,51 +199,129 @@ def my_shard(rank: int, G: int, L: int, batch_per_gpu: int):
     return {"Gp": gp, "Gb": gb, "prime_offset": rp * Lp, "L": Lp, "batch_offset": rb * Bb, "batch": Bb}
 
 
-# ------------------------------------------------------------------ reference arm
+def my_shard(rank: int, G: int, L: int, batch: int, scaling: str = "strong") -> dict:
+    return strong_shard(rank, G, L, batch) if scaling == "strong" else weak_shard(rank, G, L, batch)
 
-def cpu_oracle_sample(logn: int, L_total: int, ciphertexts: int, config_id: int, form: str = "proth"):
-    """Time the oracle (as it stands) on `ciphertexts` full-L ciphertexts
-    (fwd+inv) on all host cores, with the same prime family as the GPU arm
-    (the oracle's own scans: step 2N for "2n", step 2^32 for "proth").
-    Returns (us_per_ntt_intt, seconds, cores)."""
+
+def sample_rows(sh: dict) -> list[tuple[int, int]]:
+    """Local (b, l) rows of a shard that rank 0 checks against the oracle: the
+    first, the last, and two interior ones (deterministic)."""
+    B, L = sh["batch"], sh["L"]
+    cand = [(0, 0), (B - 1, L - 1), (B // 2, L // 2), ((B * 7) // 11, (L * 5) // 7)]
+    out = []
+    for c in cand:
+        if c not in out:
+            out.append(c)
+    return out
+
+
+# ------------------------------------------------------------------ checksums
+
+# per-row checksum of 64-bit words x_i (no overflow in int64 for N <= 2^17):
+#   s0 = sum (x_i & (2^28 - 1)) (i + 1),  s1 = sum (x_i >> 28),  s2 = sum (x_i >> 28) ((7 i + 3) & 1023)
+def row_checksums_np(rows: np.ndarray) -> np.ndarray:
+    r = rows.reshape(-1, rows.shape[-1]).astype(np.uint64)
+    N = r.shape[-1]
+    i = np.arange(N, dtype=np.int64)
+    lo = (r & np.uint64(0xFFFFFFF)).astype(np.int64)
+    hi = (r >> np.uint64(28)).astype(np.int64)
+    return np.stack([(lo * (i + 1)).sum(-1), hi.sum(-1), (hi * ((7 * i + 3) & 1023)).sum(-1)], -1)
+
+
+def row_checksums_torch(dev, B: int, L: int, N: int):
+    import torch
+    x = dev.view(B * L, N)
+    i = torch.arange(N, dtype=torch.int64, device=dev.device)
+    lo = x & 0xFFFFFFF
+    hi = torch.bitwise_right_shift(x, 28) & 0xFFFFFFFFF  # logical shift of the 64-bit word
+    return torch.stack([(lo * (i + 1)).sum(-1), hi.sum(-1), (hi * ((7 * i + 3) & 1023)).sum(-1)], -1)
+
+
+# ------------------------------------------------------------------ host info + oracle timing
+
+def host_info() -> dict:
+    model, phys = None, set()
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name") and model is None:
+                model = line.split(":", 1)[1].strip()
+            if line.startswith("physical id"):
+                phys.add(line.split(":", 1)[1].strip())
+    except OSError:
+        pass
+    return {"cpu_model": model, "sockets": max(1, len(phys)), "nproc": os.cpu_count(),
+            "cores": len(os.sched_getaffinity(0))}
+
+
+def oracle_chain(logn: int, L: int, form: str):
     import oracle
+    N = 1 << logn
+    primes = oracle.find_primes(1 << 31, L) if form == "proth" else oracle.find_primes(N, L)
+    return primes, [oracle.find_psi(p, N) for p in primes]
+
+
+def oracle_fwd_inv_seconds(x: np.ndarray, primes, psis, nthreads: int) -> float:
+    import oracle
+    t0 = time.perf_counter()
+    oracle.ntt_batch(x, primes, psis, +1, nthreads)
+    oracle.ntt_batch(x, primes, psis, -1, nthreads)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(logn: int, L: int, batch: int, cfg_id: int, form: str, reps: int = 2) -> dict:
+    """The oracle as it stands (SURVEY 8(d) "Oracle"): after a warm-up, the
+    whole job (batch ciphertexts x L primes, NTT + iNTT) on all host cores,
+    `reps` times; and one ciphertext on one core.  us per full-L ciphertext."""
     import synth
     N = 1 << logn
-    primes = oracle.find_primes(1 << 31, L_total) if form == "proth" else oracle.find_primes(N, L_total)
-    psis = [oracle.find_psi(p, N) for p in primes]
-    x = synth.rns_rows(primes, ciphertexts, N, config_id=config_id)
-    cores = len(os.sched_getaffinity(0))
-    t0 = time.perf_counter()
-    oracle.ntt_batch(x, primes, psis, +1, cores)
-    oracle.ntt_batch(x, primes, psis, -1, cores)
-    dt = time.perf_counter() - t0
-    return dt / ciphertexts * 1e6, dt, cores
+    primes, psis = oracle_chain(logn, L, form)
+    info = host_info()
+    cores = info["cores"]
+    x1 = synth.rns_rows(primes, 1, N, config_id=cfg_id)
+    oracle_fwd_inv_seconds(x1.copy(), primes, psis, cores)  # warm-up (threads, pages)
+    xb = synth.rns_rows(primes, batch, N, config_id=cfg_id)
+    ts = [oracle_fwd_inv_seconds(xb, primes, psis, cores) for _ in range(reps)]
+    one = oracle_fwd_inv_seconds(x1.copy(), primes, psis, 1)
+    T = statistics.mean(ts)
+    return {"value": round(T / batch * 1e6, 1), "unit": "us", "cores": cores, "kind": "oracle",
+            "sample": f"whole job: {batch} ciphertexts x {L} primes x N=2^{logn}, fwd+inv, {reps} reps after "
+                      f"a warm-up, {cores} threads ({T:.2f} s per rep)",
+            "one_core_us": round(one * 1e6, 1), "cpu_model": info["cpu_model"], "sockets": info["sockets"],
+            "nproc": info["nproc"]}
 
+
+# ------------------------------------------------------------------ reference arm
 
 def run_reference(args):
+    """The tier's reference arm: the oracle (the paper's algorithm written
+    plainly, CPU) as it stands, each step one whole C4 job (or the config's),
+    the same routine as the GPU arm's cpu_baseline.  Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    logn, L, batch, text = CONFIGS[args.config]
     import synth
-    cfg_id = synth.CONFIG_IDS[args.config]
+    cfg = "C4" if args.config == "C5" else args.config
+    logn, L, batch, text = CONFIGS[cfg]
+    N = 1 << logn
+    cfg_id = synth.CONFIG_IDS[cfg]
+    primes, psis = oracle_chain(logn, L, args.primes)
+    info = host_info()
+    cores = info["cores"]
+    xb = synth.rns_rows(primes, batch, N, config_id=cfg_id)
     for _ in range(args.warmup):
-        cpu_oracle_sample(logn, L, 1, cfg_id, args.primes)
-    times = []
-    cores = None
-    for _ in range(args.steps):
-        us, dt, cores = cpu_oracle_sample(logn, L, 1, cfg_id, args.primes)
-        times.append(dt)
-    T = sum(times) / len(times)
-    value = T * 1e6  # one full-L ciphertext per step
+        oracle_fwd_inv_seconds(xb, primes, psis, cores)
+    times = [oracle_fwd_inv_seconds(xb, primes, psis, cores) for _ in range(args.steps)]
+    T = statistics.mean(times)
+    value = T / batch * 1e6
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "us", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(T * 1e3, 3), "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {text}; NTT+iNTT", "N": 1 << logn, "L": L,
-                   "sample": "1 full-L ciphertext per step"},
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"{cfg}: {text}; NTT+iNTT of every row", "N": N, "L": L, "batch": batch,
+                   "primes": PRIME_TEXT[args.primes], "sample": f"the whole {cfg} job per step"},
         "cpu_baseline": {"value": round(value, 3), "unit": "us", "cores": cores, "kind": "oracle",
-                         "sample": f"1 ciphertext x {L} primes x N=2^{logn}, fwd+inv per step"},
+                         "sample": f"{batch} ciphertexts x {L} primes x N=2^{logn}, fwd+inv per step, {cores} threads",
+                         "cpu_model": info["cpu_model"], "sockets": info["sockets"], "nproc": info["nproc"]},
         "e2e": {"value": round(value, 3), "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -197,160 +329,211 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------------ self-launch
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(args) -> int:
+    """`python bench.py --gpus N` without torchrun: re-run this script under
+    torch.distributed.run with N local ranks (the driver's own launch line)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 # ------------------------------------------------------------------ own arm
 
-def run_own(args):
+def gather_rows(dist, t, world: int, dev: str):
+    """all_gather of a [rows, k] int64 tensor whose row count differs per rank
+    (ragged prime ranges): counts first, then zero-padded rows; returns every
+    rank's rows on the CPU, in rank order."""
     import torch
-    import torch.distributed as dist
+    if world == 1:
+        return [t.cpu()]
+    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=dev)
+    ns = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(ns, n)
+    m = int(max(v.item() for v in ns))
+    pad = torch.zeros((m, t.shape[1]), dtype=torch.int64, device=dev)
+    pad[: t.shape[0]] = t.to(dev)
+    outs = [torch.zeros_like(pad) for _ in range(world)]
+    dist.all_gather(outs, pad)
+    return [o[: int(k.item())].cpu() for o, k in zip(outs, ns)]
 
+
+class Dist:
+    """Rank / world / reductions.  Backend: NCCL, one rank per GPU; gloo when
+    ranks share a GPU (fewer visible devices than ranks -- tests, one-GPU
+    boxes) or BENCH_DIST_BACKEND=gloo."""
+
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        ndev = max(1, torch.cuda.device_count())
+        self.local = int(os.environ.get("LOCAL_RANK", "0")) % ndev
+        torch.cuda.set_device(self.local)
+        self.backend = os.environ.get("BENCH_DIST_BACKEND") or ("nccl" if ndev >= self.world else "gloo")
+        if self.world > 1:
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group("gloo")
+        self.dev = "cuda" if self.backend == "nccl" else "cpu"
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def allreduce(self, vals, op="max"):
+        if self.world == 1:
+            return list(vals)
+        t = self.torch.tensor(vals, dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op={"max": self.dist.ReduceOp.MAX, "min": self.dist.ReduceOp.MIN,
+                                    "sum": self.dist.ReduceOp.SUM}[op])
+        return t.tolist()
+
+    def gather_rows(self, t):
+        return gather_rows(self.dist, t, self.world, self.dev)
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+def timed_steps(D, plan, dev, steps, warmup, flush_l2=False, scratch=None, sample_clocks=False):
+    """W untimed (fwd, inv) steps, then K steps timed with CUDA events on the
+    launching stream between barriers; per-kernel times from events between
+    the ntt_launch_pass calls.  Returns (this rank's ms, per-kernel ms, clocks, launches)."""
+    from paper_2012_01968_b200 import NTT_DIR_FORWARD, NTT_DIR_INVERSE
+    torch = D.torch
+    stream = torch.cuda.current_stream()
+    passes = plan.passes
+    seq = [(NTT_DIR_FORWARD, i) for i in range(passes)] + [(NTT_DIR_INVERSE, i) for i in range(passes)]
+    for _ in range(warmup):
+        plan.forward(dev)
+        plan.inverse(dev)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(seq) + 1)] for _ in range(steps)]
+    D.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(D.local) if sample_clocks else None
+    if sampler:
+        sampler.__enter__()
+    start.record(stream)
+    for s in range(steps):
+        if flush_l2:
+            scratch.fill_(s)  # untimed: between ev[s-1][-1] and ev[s][0]
+        ev[s][0].record(stream)
+        for j, (d, p) in enumerate(seq):
+            plan.launch_pass(dev, d, p)
+            ev[s][j + 1].record(stream)
+    end.record(stream)
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.__exit__()
+    D.barrier()
+    if flush_l2:  # the sum of the per-step spans, flushes excluded
+        ms = sum(ev[s][0].elapsed_time(ev[s][-1]) for s in range(steps))
+    else:
+        ms = start.elapsed_time(end)
+    per_kernel = [statistics.mean(ev[s][j].elapsed_time(ev[s][j + 1]) for s in range(steps)) for j in range(len(seq))]
+    names = [("fwd" if d == NTT_DIR_FORWARD else "inv") + f"_pass{p}" for d, p in seq]
+    return ms, dict(zip(names, per_kernel)), (sampler.summary() if sampler else None), len(seq) * steps
+
+
+def modmuls_per_launch(name: str, rows: int, N: int, logn: int, log_n1: int, passes: int, ots: int = 0) -> int:
+    """Shoup modmuls of one kernel launch: one per butterfly,
+    + N/2 per OT stage (the second factor), + N/2 for the fused N^-1 (the last
+    inverse stage multiplies both outputs)."""
+    if passes == 2:
+        st = {"fwd_pass0": log_n1, "fwd_pass1": logn - log_n1, "inv_pass0": logn - log_n1, "inv_pass1": log_n1}[name]
+        ot_here = name in ("fwd_pass1", "inv_pass0")
+        last_inv = name == "inv_pass1"
+    else:
+        st, ot_here, last_inv = logn, True, name.startswith("inv")
+    per_row = (N // 2) * st + (N // 2) * (ots if ot_here else 0) + (N // 2 if last_inv else 0)
+    return rows * per_row
+
+
+def transform_line(D, args, logn, L_total, batch_job, text):
+    """C1-C4: time the job, verify, and build rank 0's line."""
+    torch = D.torch
     import synth
     from paper_2012_01968_b200 import NTT_DIR_FORWARD, NTT_DIR_INVERSE, Plan, find_primes
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus N>1 needs torchrun --nproc-per-node N")
-    # BENCH_DIST_BACKEND=gloo (testing only): several ranks sharing the visible
-    # GPUs, reductions on CPU tensors; the default is one rank per GPU over NCCL.
-    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
-    local = local % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(local)
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-    red_dev = "cuda" if backend == "nccl" else "cpu"
-
-    logn, L_total, batch_per_gpu, text = CONFIGS[args.config]
+    rank, world = D.rank, D.world
     N = 1 << logn
-    sh = my_shard(rank, world, L_total, batch_per_gpu)
-    all_primes = find_primes(N, L_total, args.primes)
-    primes = all_primes[sh["prime_offset"]: sh["prime_offset"] + sh["L"]]
-    L, B = sh["L"], sh["batch"]
-    words = B * L * N
+    sh = my_shard(rank, world, L_total, batch_job, args.scaling)
+    units = batch_job if args.scaling == "strong" else batch_job * world  # full-L ciphertexts per step
     cfg_id = synth.CONFIG_IDS[args.config]
 
-    # inputs: seeded residues, pinned host (for e2e) and device-resident (for value)
-    host = torch.empty(words, dtype=torch.int64).pin_memory()
-    synth.rns_rows(primes, B, N, config_id=cfg_id, prime_offset=sh["prime_offset"], L_total=L_total,
-                   batch_offset=sh["batch_offset"], out=host.numpy().view(np.uint64).reshape(B, L, N))
-    dev = host.cuda()
-    ref_sum = None
+    def make_inputs(form):
+        primes = find_primes(N, L_total, form)[sh["prime_offset"]: sh["prime_offset"] + sh["L"]]
+        host = torch.empty(sh["batch"] * sh["L"] * N, dtype=torch.int64).pin_memory()
+        synth.rns_rows(primes, sh["batch"], N, config_id=cfg_id, prime_offset=sh["prime_offset"], L_total=L_total,
+                       batch_offset=sh["batch_offset"],
+                       out=host.numpy().view(np.uint64).reshape(sh["batch"], sh["L"], N))
+        return primes, host
 
-    # Inputs smaller than 2x L2 (C1, C2): flush L2 between timed steps by writing a
-    # 256 MiB scratch buffer, outside the timed spans (timing rule); C3/C4 inputs
-    # are larger than L2 and run back to back.
-    L2_BYTES = 126 * 2**20
+    B, L = sh["batch"], sh["L"]
+    rows = B * L
+    words = rows * N
+    primes, host = make_inputs(args.primes)
+    dev = host.cuda()
     flush_l2 = words * 8 < 2 * L2_BYTES
     scratch = torch.empty(256 * 2**20 // 4, dtype=torch.int32, device="cuda") if flush_l2 else None
 
-    def timed(plan, steps, warmup):
-        stream = torch.cuda.current_stream()
-        passes = plan.passes
-        seq = [(NTT_DIR_FORWARD, i) for i in range(passes)] + [(NTT_DIR_INVERSE, i) for i in range(passes)]
-        for _ in range(warmup):
-            plan.forward(dev)
-            plan.inverse(dev)
-        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(seq) + 1)] for _ in range(steps)]
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        sampler = ClockSampler(local)
-        with sampler:
-            start.record(stream)
-            for s in range(steps):
-                if flush_l2:
-                    scratch.fill_(s)  # untimed: between ev[s-1][-1] and ev[s][0]
-                ev[s][0].record(stream)
-                for j, (d, p) in enumerate(seq):
-                    plan.launch_pass(dev, d, p)
-                    ev[s][j + 1].record(stream)
-            end.record(stream)
-            torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        if flush_l2:  # the sum of the per-step spans, flushes excluded
-            ms = sum(ev[s][0].elapsed_time(ev[s][-1]) for s in range(steps))
-        else:
-            ms = start.elapsed_time(end)
-        per_kernel = [statistics.mean(ev[s][j].elapsed_time(ev[s][j + 1]) for s in range(steps))
-                      for j in range(len(seq))]
-        if world > 1:
-            t = torch.tensor([ms], device=red_dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        names = [("fwd" if d == NTT_DIR_FORWARD else "inv") + f"_pass{p}" for d, p in seq]
-        return ms, dict(zip(names, per_kernel)), sampler.summary(), len(seq) * steps
-
     plan = Plan(N, primes)
     info = plan.info()
-    ms, kern, clocks, launches = timed(plan, args.steps, args.warmup)
-    # the roundtrip restores the input exactly: a free correctness check
+    ms, kern, clocks, launches = timed_steps(D, plan, dev, args.steps, args.warmup, flush_l2, scratch, True)
+    ms_step_rank = ms / args.steps
+
+    # ---- verification (untimed): the roundtrip restored every row; then one
+    # forward, per-row checksums gathered to rank 0, checked against the oracle
     torch.cuda.synchronize()
     ok_roundtrip = bool(torch.equal(dev, host.cuda()))
+    plan.forward(dev)
+    cs = row_checksums_torch(dev, B, L, N)
+    plan.inverse(dev)
+    torch.cuda.synchronize()
+    ok_roundtrip = ok_roundtrip and bool(torch.equal(dev, host.cuda()))
+    gathered = D.gather_rows(cs)
+    per_rank_ms = [0.0] * world
+    per_rank_ms[rank] = ms_step_rank
+    per_rank_ms = D.allreduce(per_rank_ms, "sum")
+    ms_step = max(per_rank_ms)  # the job's step time: max over ranks (device time)
+    ok_roundtrip = bool(D.allreduce([float(ok_roundtrip)], "min")[0])
 
-    ms_step = ms / args.steps
-    units = batch_per_gpu * world  # full-L ciphertexts the whole job processed per step
-    value_us = ms_step * 1e3 / units
-    rows = B * L
-    bytes_alg = 2 * 2 * 8 * N * rows  # compulsory: read+write each word once, fwd and inv
-    hbm_peak, peak_kind = peaks()
-    dom = max(kern, key=kern.get)
-    dom_ms = kern[dom]
-    bfly_per_launch = rows * (N // 2) * (logn // 2 if plan.passes == 2 else logn)
-    # stages per kernel: Kernel-1 holds log N1, Kernel-2 log N2
-    if plan.passes == 2:
-        ln1 = info["log_n1"]
-        st = {"fwd_pass0": ln1, "fwd_pass1": logn - ln1, "inv_pass0": logn - ln1, "inv_pass1": ln1}[dom]
-    else:
-        st = logn
-    bfly_per_launch = rows * (N // 2) * st
-    achieved = bfly_per_launch / (dom_ms * 1e-3) / 1e9
-    form = args.primes if info.get("proth") else "2n"
-    peak = alu_peak(form)
-    dom_bytes = 2 * 8 * N * rows  # compulsory bytes of one pass: read + write every word
-    hbm_dom = dom_bytes / (dom_ms * 1e-3) / 1e9
-    traffic = None
-    tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tr_path):
-        try:
-            traffic = json.load(open(tr_path)).get(dom)
-        except Exception:
-            traffic = None
-
-    # the paper's two-kernel split (two HBM passes per direction), same primes and inputs
-    tk_plan = Plan(N, primes, fused=False)
-    tk_steps = max(3, args.steps // 2)
-    ms_tk, kern_tk, _, _ = timed(tk_plan, tk_steps, 2)
-    tk_plan.close()
-
-    # the other prime family, same workload, reported beside
-    alt_form = "2n" if args.primes == "proth" else "proth"
-    alt_primes = find_primes(N, L_total, alt_form)[sh["prime_offset"]: sh["prime_offset"] + sh["L"]]
-    alt_host = torch.empty(words, dtype=torch.int64)
-    synth.rns_rows(alt_primes, B, N, config_id=cfg_id, prime_offset=sh["prime_offset"], L_total=L_total,
-                   batch_offset=sh["batch_offset"], out=alt_host.numpy().view(np.uint64).reshape(B, L, N))
-    dev.copy_(alt_host.cuda())
+    # ---- the other prime family at equal rank, OT on, the negacyclic product, e2e
+    alt_form = "proth" if args.primes == "2n" else "2n"
+    alt_primes, alt_host = make_inputs(alt_form)
+    alt_dev = alt_host.cuda()
     alt_plan = Plan(N, alt_primes)
     alt_steps = max(3, args.steps // 2)
-    ms_alt, kern_alt, _, _ = timed(alt_plan, alt_steps, 2)
-    alt_ok = bool(torch.equal(dev, alt_host.cuda()))
-    alt_proth = alt_plan.info()["proth"]
+    ms_alt, kern_alt, _, _ = timed_steps(D, alt_plan, alt_dev, alt_steps, 2, flush_l2, scratch)
+    torch.cuda.synchronize()
+    alt_ok = bool(D.allreduce([float(torch.equal(alt_dev, alt_host.cuda()))], "min")[0])
+    alt_ms_step = max(D.allreduce([ms_alt / alt_steps], "max"))
+    alt_info = alt_plan.info()
+    alt_key = "proth" if alt_info["arith"] == "proth" else "2n"
     alt_plan.close()
-    del alt_host
-    dev.copy_(host.cuda())
+    del alt_dev, alt_host
 
-    # OT on: same workload, reported beside (north_star: OT on/off)
     ot_plan = Plan(N, primes, ot=True)
-    ms_ot, kern_ot, _, _ = timed(ot_plan, max(3, args.steps // 2), 2)
-    ot_plan.close()
     ot_steps = max(3, args.steps // 2)
+    ms_ot, kern_ot, _, _ = timed_steps(D, ot_plan, dev, ot_steps, 2, flush_l2, scratch)
+    ot_ms_step = max(D.allreduce([ms_ot / ot_steps], "max"))
+    ot_stages = ot_plan.info()["ot_stages"]
+    ot_plan.close()
 
-    # NEXT-2 context: negacyclic product of two full-L ciphertext batches (fwd a, fwd b, fused odot+inv)
     pm_steps = max(2, min(args.steps, 5))
     other = dev.clone()
     for _ in range(2):
@@ -362,7 +545,7 @@ def run_own(args):
         plan.negacyclic_mul(other, dev)
     e1.record()
     torch.cuda.synchronize()
-    pm_ms = e0.elapsed_time(e1) / pm_steps
+    pm_ms = max(D.allreduce([e0.elapsed_time(e1) / pm_steps], "max"))
     del other
     dev.copy_(host.cuda())
 
@@ -371,92 +554,281 @@ def run_own(args):
     ws = torch.empty(plan.workspace_words(B), dtype=torch.int64, device="cuda")
     plan.execute_host(host, out_host, NTT_DIR_FORWARD | NTT_DIR_INVERSE, ws)  # warm
     e2e_steps = max(2, min(args.steps, 5))
-    if world > 1:
-        dist.barrier()
+    D.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         plan.execute_host(host, out_host, NTT_DIR_FORWARD | NTT_DIR_INVERSE, ws)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    if world > 1:
-        t = torch.tensor([e2e_s], device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_ok = bool(torch.equal(out_host, host))
-    if world > 1:  # every rank's exactness flags to rank 0 (NCCL carries verification, not data)
-        t = torch.tensor([int(ok_roundtrip), int(e2e_ok)], device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        ok_roundtrip, e2e_ok = bool(t[0].item()), bool(t[1].item())
+    e2e_s = max(D.allreduce([(time.perf_counter() - t0) / e2e_steps], "max"))
+    e2e_ok = bool(D.allreduce([float(torch.equal(out_host, host))], "min")[0])
     del ws
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        us, dt, cores = cpu_oracle_sample(logn, L_total, 1, cfg_id, args.primes)
-        cpu = {"value": round(us, 1), "unit": "us", "cores": cores, "kind": "oracle",
-               "sample": f"1 ciphertext x {L_total} primes x N=2^{logn}, fwd+inv ({dt:.2f} s)"}
+    if rank != 0:
+        plan.close()
+        return None
 
-    if rank == 0:
-        line = {
-            "metric": METRIC,
-            "value": round(value_us, 3),
-            "unit": "us",
-            "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": round(ms_step, 4),
-            "higher_is_better": False,
-            "scaling": "weak",
-            "vs_baseline": None,
-            "dtype": "u64",
-            "data": "synthetic: seeded splitmix64 residues uniform mod each prime (synth/)",
-            "config": {
-                "workload": f"{args.config}: {text} per GPU; one step = NTT + iNTT of every row",
-                "N": N, "L": L_total, "batch_per_gpu": batch_per_gpu, "global_batch": units,
-                "shard": f"{sh['Gp']} prime ranges x {sh['Gb']} ciphertext ranges",
-                "log_n1": info["log_n1"], "passes": info["passes"], "cluster": info["cluster"], "ot": False,
-                "primes": {"2n": "p = 1 mod 2N descending from 2^60 - 2N + 1 (DESIGN.md R3)",
-                           "proth": "p = 1 mod 2^32 descending from 2^60 - 2^32 + 1 (DESIGN.md 5.1)"}[args.primes],
-                "proth_arith": bool(info.get("proth")),
-                "l2": ("L2 flushed between timed steps (256 MiB write, untimed; inputs %.0f MiB per GPU)" if flush_l2
-                       else "inputs larger than L2 (%.0f MiB per GPU vs 126 MB L2)") % (words * 8 / 2**20),
+    # ---- rank 0: check sampled rows of every rank against the oracle
+    import oracle
+    checked, bad = 0, []
+    chain_primes, chain_psis = oracle_chain(logn, L_total, args.primes)
+    for r in range(world):
+        shr = my_shard(r, world, L_total, batch_job, args.scaling)
+        cs_r = gathered[r].numpy()
+        for (b, l) in sample_rows(shr):
+            gl = shr["prime_offset"] + l
+            x = synth.rns_rows([chain_primes[gl]], 1, N, config_id=cfg_id, prime_offset=gl, L_total=L_total,
+                               batch_offset=shr["batch_offset"] + b)
+            want = row_checksums_np(oracle.ntt_batch(x, [chain_primes[gl]], [chain_psis[gl]], +1))[0]
+            checked += 1
+            if not np.array_equal(cs_r[b * shr["L"] + l], want):
+                bad.append([r, shr["batch_offset"] + b, gl])
+
+    value_us = ms_step * 1e3 / units
+    hbm_peak, peak_kind = peaks()
+    ceil = butterfly_ceiling()
+    form = info["arith"] if info["arith"] == "proth" else "2n"
+
+    def roofline_of(kern_ms, form_, ots=0):
+        dom = max(kern_ms, key=kern_ms.get)
+        mm = modmuls_per_launch(dom, rows, N, logn, info["log_n1"], plan.passes, ots)
+        ach = mm / (kern_ms[dom] * 1e-3) / 1e9
+        peak = alu_peak(form_)
+        c = ceil.get(("ct_" if dom.startswith("fwd") else "gs_") + form_)
+        return dom, mm, ach, peak, c
+
+    dom, mm, achieved, peak, c_dom = roofline_of(kern, form)
+    dom_bytes = 2 * 8 * N * rows  # compulsory bytes of one pass: read + write every word
+    per_kernel = {}
+    for k, t in kern.items():
+        m = modmuls_per_launch(k, rows, N, logn, info["log_n1"], plan.passes)
+        g = m / (t * 1e-3) / 1e9
+        cc = ceil.get(("ct_" if k.startswith("fwd") else "gs_") + form)
+        per_kernel[k] = {"ms": round(t, 4), "modmuls": m, "Gmodmul_s": round(g, 1), "frac_of_peak": round(g / peak, 4),
+                         "frac_of_ceiling": round(g / cc, 4) if cc else None,
+                         "hbm_gbs": round(dom_bytes / (t * 1e-3) / 1e9, 1)}
+    traffic, traffic_src = None, None
+    tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            tr = json.load(open(tr_path))
+            if tr.get("primes") == args.primes and tr.get("config") == args.config and args.scaling == "strong" \
+                    and world == 1:
+                traffic = tr["kernels"].get(dom)
+                traffic_src = {k: tr.get(k) for k in ("file", "commit", "primes", "config")}
+        except Exception:
+            traffic = None
+    # step-level HBM fractions and the ceilings of section 5.4
+    ct_bytes = lambda per_row: per_row * N * L_total  # bytes per full-L ciphertext
+    two_pass_step = 2 * 2 * 16  # 2 directions x 2 passes x (read + write 8 B)
+    step_modmuls_ct = L_total * ((N // 2) * logn * 2 + N // 2)
+    cc_ct, cc_gs = ceil.get("ct_" + form), ceil.get("gs_" + form)
+    floor_us = None
+    if cc_ct and cc_gs:
+        floor_us = (L_total * (N // 2) * logn / cc_ct + L_total * ((N // 2) * logn + N // 2) / cc_gs) / 1e3
+    line = {
+        "metric": METRIC,
+        "value": round(value_us, 3),
+        "unit": "us",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": False,
+        "scaling": "strong" if args.scaling == "strong" else "weak",
+        "vs_baseline": None,
+        "dtype": "u64",
+        "data": "synthetic: seeded splitmix64 residues uniform mod each prime (synth/)",
+        "config": {
+            "workload": f"{args.config}: {text}; one step = NTT + iNTT of every row of the job",
+            "N": N, "L": L_total, "global_batch": units,
+            "shard": (f"contiguous prime ranges {[n for _, n in prime_ranges(world, L_total)]}, all "
+                      f"{batch_job} ciphertexts per rank" if args.scaling == "strong"
+                      else f"{sh['Gp']} prime ranges x {sh['Gb']} ciphertext ranges, {batch_job} ciphertexts per GPU"),
+            "parallelism": f"prime-sharded x{world}" if world > 1 else "1 GPU",
+            "log_n1": info["log_n1"], "passes": info["passes"], "ot": False,
+            "primes": PRIME_TEXT[args.primes], "arith": info["arith"],
+            "l2": ("L2 flushed between timed steps (256 MiB write, untimed; inputs %.0f MiB per GPU)" % (words * 8 / 2**20)
+                   if flush_l2 else "inputs larger than L2 (%.0f MiB per GPU vs 126 MB L2)" % (words * 8 / 2**20)),
+            "dist_backend": D.backend if world > 1 else None,
+        },
+        "residue_ntts_per_s": round(2 * units * L_total / (ms_step * 1e-3), 1),
+        "per_rank_ms": [round(v, 4) for v in per_rank_ms],
+        "imbalance": round(max(per_rank_ms) / min(per_rank_ms), 4),
+        "verify": {"rows_checked_vs_oracle": checked, "mismatched": bad, "verified_rows": checked - len(bad),
+                   "roundtrip_exact_all_rows": ok_roundtrip,
+                   "how": "after timing: one forward, per-row checksums all_gathered to rank 0, sampled rows of "
+                          "every rank recomputed by the oracle; inverse restores every row exactly"},
+        "roofline": {
+            "bound": "alu", "kernel": dom, "achieved": round(achieved, 1), "peak": round(peak, 1),
+            "unit": "Gmodmul/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+            "traffic_source": traffic_src,
+            "units": f"{mm} Shoup modmuls per launch of {dom} (SURVEY 8(d): one per butterfly, "
+                     "+N/2 per row for the fused N^-1)",
+            "peak_kind": "derived: multiply-pipe clk per Shoup modmul (IMAD 2 clk per guide; IMAD.WIDE 5.33, "
+                         "IMAD.HI 4.57 clk measured) x 148 SMs x 1.965 GHz (DESIGN.md 7)",
+            "ceiling": {"value": c_dom, "unit": "Gbutterfly/s",
+                        "what": "the kernels' own butterflies in a register-only loop, measured live "
+                                "(tools/libs/bf_roof, 32 warps/SM, no memory)", "all": ceil},
+            "frac_of_ceiling": round(achieved / c_dom, 4) if c_dom else None,
+            "hbm": {"achieved": round(dom_bytes / (kern[dom] * 1e-3) / 1e9, 1), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(dom_bytes / (kern[dom] * 1e-3) / 1e9 / hbm_peak, 4), "peak_kind": peak_kind,
+                    "bytes": "compulsory 16N per row per pass"},
+            "step": {
+                "hbm_two_pass_gbs": round(ct_bytes(two_pass_step) * units / (ms_step * 1e-3) / 1e9, 1),
+                "hbm_two_pass_frac": round(ct_bytes(two_pass_step) * units / (ms_step * 1e-3) / 1e9 / hbm_peak, 4),
+                "hbm_compulsory_frac": round(ct_bytes(32) * units / (ms_step * 1e-3) / 1e9 / hbm_peak, 4),
+                "modmuls_per_ciphertext": step_modmuls_ct,
             },
-            "residue_ntts_per_s": round(2 * rows * world / (ms_step * 1e-3), 1),
-            "hbm_gbs_compulsory": round(bytes_alg / (ms_step * 1e-3) / 1e9, 1),
-            "roofline": {
-                "bound": "alu", "kernel": dom, "achieved": round(achieved, 1), "peak": round(peak, 1),
-                "unit": "Gbutterfly/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                "peak_kind": "derived: multiply-pipe clk per Shoup butterfly (IMAD 2 clk per guide; IMAD.WIDE 5.33, "
-                             "IMAD.HI 4.57 clk measured) x 148 SMs x 1.965 GHz (DESIGN.md 7)",
-                "peak_nominal_quarter_rate": round(alu_peak(form, nominal=True), 1),
-                "hbm": {"achieved": round(hbm_dom, 1), "peak": hbm_peak, "unit": "GB/s",
-                        "frac": round(hbm_dom / hbm_peak, 4), "peak_kind": peak_kind,
-                        "bytes": "compulsory 16N per row per pass"},
+            "target": {
+                "hbm_frac": 0.70,
+                "us_per_ciphertext_needed": round(ct_bytes(two_pass_step) / (0.70 * hbm_peak * 1e9) * 1e6, 1),
+                "butterfly_ceiling_floor_us": round(floor_us, 1) if floor_us else None,
+                "note": "a two-pass step at 70% of HBM needs the first number; the kernels' own butterflies at "
+                        "their register-only rate (CT for forward, GS for inverse) need the second",
             },
-            "kernels_ms": {k: round(v, 4) for k, v in kern.items()},
-            "two_kernel": {"value": round(ms_tk / tk_steps * 1e3 / units, 3), "unit": "us",
-                           "ms_per_step": round(ms_tk / tk_steps, 4),
-                           "kernels_ms": {k: round(v, 4) for k, v in kern_tk.items()}},
-            "other_primes": {"primes": alt_form, "proth_arith": alt_proth,
-                             "value": round(ms_alt / alt_steps * 1e3 / units, 3), "unit": "us",
-                             "ms_per_step": round(ms_alt / alt_steps, 4), "roundtrip_exact": alt_ok,
-                             "kernels_ms": {k: round(v, 4) for k, v in kern_alt.items()}},
-            "ot_on": {"value": round(ms_ot / ot_steps * 1e3 / units, 3), "unit": "us",
-                      "ms_per_step": round(ms_ot / ot_steps, 4),
-                      "kernels_ms": {k: round(v, 4) for k, v in kern_ot.items()}},
-            "negacyclic_mul": {"ms_per_step": round(pm_ms, 4), "us_per_ct": round(pm_ms * 1e3 / units, 3),
-                               "what": "b <- a*b mod (X^N+1): 2 forward NTTs + fused odot/inverse, per ciphertext pair"},
-            "cpu_baseline": cpu,
-            "e2e": {"value": round(e2e_s * 1e6 / units, 3), "unit": "us",
-                    "h2d_bytes_per_step": words * 8, "d2h_bytes_per_step": words * 8,
-                    "ms_per_step": round(e2e_s * 1e3, 3), "ok": e2e_ok},
-            "gpu_launches": launches,
-            "clocks": clocks,
-            "roundtrip_exact": ok_roundtrip,
-        }
-        print(json.dumps(line), flush=True)
+            "per_kernel": per_kernel,
+        },
+        "kernels_ms": {k: round(v, 4) for k, v in kern.items()},
+        alt_form: {"primes": PRIME_TEXT[alt_form], "arith": alt_info["arith"],
+                   "value": round(alt_ms_step * 1e3 / units, 3), "unit": "us",
+                   "ms_per_step": round(alt_ms_step, 4), "roundtrip_exact": alt_ok,
+                   "kernels_ms": {k: round(v, 4) for k, v in kern_alt.items()},
+                   "roofline_frac": round(roofline_of(kern_alt, alt_key)[2] / alu_peak(alt_key), 4),
+                   "frac_of_ceiling": (round(roofline_of(kern_alt, alt_key)[2] / roofline_of(kern_alt, alt_key)[4], 4)
+                                       if roofline_of(kern_alt, alt_key)[4] else None)},
+        "ot_on": {"value": round(ot_ms_step * 1e3 / units, 3), "unit": "us", "ms_per_step": round(ot_ms_step, 4),
+                  "ot_stages": ot_stages, "kernels_ms": {k: round(v, 4) for k, v in kern_ot.items()}},
+        "negacyclic_mul": {"ms_per_step": round(pm_ms, 4), "us_per_ct": round(pm_ms * 1e3 / units, 3),
+                           "what": "b <- a*b mod (X^N+1): 2 forward NTTs + fused odot/inverse, per ciphertext pair"},
+        "cpu_baseline": None,
+        "e2e": {"value": round(e2e_s * 1e6 / units, 3), "unit": "us",
+                "h2d_bytes_per_step": units * L_total * N * 8, "d2h_bytes_per_step": units * L_total * N * 8,
+                "ms_per_step": round(e2e_s * 1e3, 3), "ok": e2e_ok,
+                "what": "ntt_execute_host: pinned host in -> H2D -> fwd -> inv -> D2H, every rank its shard"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "roundtrip_exact": ok_roundtrip,
+    }
     plan.close()
-    if world > 1:
-        dist.destroy_process_group()
-    return 0
+    return line
+
+
+def c5_line(D, args):
+    """C5, the mixed request stream at N = 2^16 (BASELINE config 5):
+    per L, throughput mode (requests round-robin to ranks, each rank's
+    requests of one L batched into one call) and latency mode (one request at
+    a time, its primes sharded over the ranks, replayed from a request
+    graph).  value = mixed-stream latency-mode us per request (the mean over
+    the L sweep, one request per L in turn)."""
+    torch = D.torch
+    import synth
+    from paper_2012_01968_b200 import NTT_DIR_FORWARD, NTT_DIR_INVERSE, Plan, find_primes
+
+    rank, world = D.rank, D.world
+    logn = 16
+    N = 1 << logn
+    cfg_id = synth.CONFIG_IDS["C5"]
+    sweep, launches = {}, 0
+    ok_all = True
+    for L in C5_LS:
+        primes_all = find_primes(N, L, args.primes)
+        # throughput: requests r = rank, rank + world, ... ; all of this rank's requests share the chain -> one batch
+        mine = list(range(rank, C5_REQUESTS, world))
+        tp_plan = Plan(N, primes_all)
+        x = torch.empty(len(mine) * L * N, dtype=torch.int64)
+        synth.rns_rows(primes_all, len(mine), N, config_id=cfg_id, out=x.numpy().view(np.uint64).reshape(len(mine), L, N))
+        xd = x.cuda()
+        ref = xd.clone()
+        for _ in range(args.warmup):
+            tp_plan.forward(xd)
+            tp_plan.inverse(xd)
+        D.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            tp_plan.forward(xd)
+            tp_plan.inverse(xd)
+        e1.record()
+        torch.cuda.synchronize()
+        tp_ms = max(D.allreduce([e0.elapsed_time(e1) / args.steps], "max"))
+        launches += 2 * tp_plan.passes * args.steps
+        ok_all = ok_all and bool(torch.equal(xd, ref))
+        tp_plan.close()
+        # latency: this rank's prime range of ONE request, replayed from a request graph
+        off, n = prime_ranges(world, L)[rank] if world <= L else ((rank, 1) if rank < L else (0, 0))
+        lat_ms = 0.0
+        if n > 0:
+            lp = Plan(N, primes_all[off: off + n])
+            y = torch.empty(n * N, dtype=torch.int64)
+            synth.rns_rows(primes_all[off: off + n], 1, N, config_id=cfg_id, prime_offset=off, L_total=L,
+                           out=y.numpy().view(np.uint64).reshape(1, n, N))
+            yd = y.cuda()
+            yref = yd.clone()
+            g = lp.graph(yd, NTT_DIR_FORWARD | NTT_DIR_INVERSE)
+            for _ in range(max(3, args.warmup)):
+                g.launch()
+            reps = max(20, args.steps * 4)
+            D.barrier()
+            torch.cuda.synchronize()
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+            evs[0].record()
+            for i in range(reps):  # one request in flight: each replay waits for the previous on the stream
+                g.launch()
+                evs[i + 1].record()
+            torch.cuda.synchronize()
+            lat_ms = statistics.median(evs[i].elapsed_time(evs[i + 1]) for i in range(reps))
+            launches += reps * 2 * lp.passes
+            ok_all = ok_all and bool(torch.equal(yd, yref))
+            g.close()
+            lp.close()
+        else:
+            D.barrier()
+        lat_ms = max(D.allreduce([lat_ms], "max"))
+        sweep[str(L)] = {"throughput_us_per_request": round(tp_ms * 1e3 / C5_REQUESTS, 3),
+                         "latency_us_per_request": round(lat_ms * 1e3, 3),
+                         "latency_primes_per_rank": [c for _, c in prime_ranges(world, L)] if world <= L
+                         else [1 if r < L else 0 for r in range(world)]}
+    ok_all = bool(D.allreduce([float(ok_all)], "min")[0])
+    if rank != 0:
+        return None
+    lat_mean = statistics.mean(v["latency_us_per_request"] for v in sweep.values())
+    tp_mean = statistics.mean(v["throughput_us_per_request"] for v in sweep.values())
+    return {
+        "metric": METRIC, "value": round(lat_mean, 3), "unit": "us", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(lat_mean * len(C5_LS) / 1e3, 4), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic: seeded splitmix64 residues uniform mod each prime (synth/)",
+        "config": {"workload": "C5: mixed ciphertext stream, N=2^16, one request = NTT + iNTT of one ciphertext of "
+                               f"L primes, L in {C5_LS}; value = latency mode, mean over the sweep",
+                   "N": N, "requests_per_L_throughput": C5_REQUESTS, "primes": PRIME_TEXT[args.primes],
+                   "parallelism": f"x{world}" if world > 1 else "1 GPU"},
+        "sweep": sweep,
+        "throughput_mode_mean_us_per_request": round(tp_mean, 3),
+        "roundtrip_exact": ok_all,
+        "gpu_launches": launches,
+        "e2e": None,
+        "cpu_baseline": None,
+    }
+
+
+def run_own(args):
+    D = Dist()
+    if D.world != args.gpus and D.rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {D.world}", file=sys.stderr)
+    if args.config == "C5":
+        line = c5_line(D, args)
+    else:
+        logn, L_total, batch, text = CONFIGS[args.config]
+        line = transform_line(D, args, logn, L_total, batch, text)
+    if D.rank == 0 and line is not None:
+        if D.world == 1 and not args.no_cpu and args.config != "C5":
+            import synth
+            logn, L_total, batch, _ = CONFIGS[args.config]
+            line["cpu_baseline"] = cpu_baseline(logn, L_total, batch, synth.CONFIG_IDS[args.config], args.primes)
+        print(json.dumps(line), flush=True)
+    D.close()
+    bad = line is not None and (line.get("verify", {}).get("mismatched") or not line.get("roundtrip_exact", True))
+    return 1 if bad else 0
 
 
 def main():
@@ -465,15 +837,18 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
-    ap.add_argument("--primes", default="proth", choices=["2n", "proth"],
-                    help="prime family: proth = p = 1 mod 2^32 (default), 2n = DESIGN.md R3")
+    ap.add_argument("--primes", default="2n", choices=["2n", "proth"],
+                    help="prime chain: 2n = SURVEY 8(c)#3 (default), proth = p = 1 mod 2^32")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args)
     return run_own(args)
 
 

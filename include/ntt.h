@@ -10,9 +10,14 @@
  *    plain host or device pointers as stated per argument; sizes are unsigned.
  *  - Every function returns an ntt_status_t.  Argument errors are detected
  *    synchronously, before anything is enqueued, and leave all buffers
- *    untouched.  A CUDA launch failure is reported as NTT_ERR_CUDA (from
- *    cudaPeekAtLastError); asynchronous faults surface at the caller's next
+ *    untouched.  A CUDA launch failure is reported once as NTT_ERR_CUDA (the
+ *    library consumes it with cudaGetLastError, so it does not poison later
+ *    calls); asynchronous faults surface at the caller's next
  *    synchronisation, as for any CUDA library.
+ *  - batch * L * N1 (N1 = 2^log_n1 of the split, 1 for one kernel per row)
+ *    must be below 2^31 on every call that enqueues work, else INVALID_ARG.
+ *  - Every entry point may be called from any number of host threads; the
+ *    library's one-time per-device kernel setup is internally synchronised.
  *  - A plan is immutable after ntt_plan_create; concurrent ntt_forward /
  *    ntt_inverse calls with one plan on different streams and disjoint buffers
  *    are safe.  ntt_plan_destroy requires all work using the plan to be done.
@@ -36,7 +41,7 @@ typedef struct ntt_plan_s *ntt_plan_t;
 typedef enum {
     NTT_OK = 0,
     NTT_ERR_INVALID_N = -1,       /* N not a power of two in [2^1, 2^17] */
-    NTT_ERR_INVALID_PRIME = -2,   /* not prime, not = 1 mod 2N, >= 2^60, or repeated */
+    NTT_ERR_INVALID_PRIME = -2,   /* not prime, not = 1 mod 2N, outside [2^59, 2^60), or repeated */
     NTT_ERR_INVALID_ARG = -3,     /* null pointer, bad option value */
     NTT_ERR_MISALIGNED = -4,      /* data pointer not 16-byte aligned */
     NTT_ERR_WRONG_DEVICE = -5,    /* data pointer not on the plan's device */
@@ -55,10 +60,11 @@ typedef struct {
     unsigned ot_stages;  /* 1 or 2 (fig:3point c); 0 = 2 */
     unsigned log_n1;     /* two-kernel split N = N1*N2, log2 N1;
                             0 = automatic; ignored when one kernel holds the row */
-    int proth_arith;     /* 0 = automatic: when EVERY prime is = 1 mod 2^32 the
-                            kernels form lo64(q p) of Shoup's modmul
-                            as q + (q0 p1 << 32); -1 = always the
-                            general arithmetic.  Results are identical either way. */
+    int prime_arith;     /* 0 = automatic: when EVERY prime is = 1 mod 2^32
+                            ("Proth") the kernels form lo64(q p) of Shoup's
+                            modmul as q + (q0 p1 << 32) (DESIGN.md
+                            5.1); -1 = always the general arithmetic.  Results
+                            are identical either way. */
     int fused;           /* single pass per direction for N = 2^14..2^17: one
                             thread-block cluster of N/2^13 CTAs holds the row in
                             distributed shared memory, so each word crosses HBM
@@ -68,6 +74,15 @@ typedef struct {
                             the path is bound by the multiply pipe, not HBM --
                             DESIGN.md 5.5), 1 = on (NTT_ERR_INVALID_ARG if N is
                             outside 2^14..2^17, OT is on or log_n1 is given). */
+    int k1_variant;      /* Kernel-1 form (experiments): 0 = default
+                            (4: one 16-column tile per CTA), 5 = persistent
+                            cp.async-pipelined.  Other values: INVALID_ARG. */
+    int k2_variant;      /* Kernel-2 form: 0 = default (9: shared-twiddle CTA per
+                            block position, remainder-last schedule), 7 = the same
+                            remainder-first, 5 = persistent pipelined radix 16,
+                            6 = persistent radix 8, 3 / 4 = one-shot radix 8 / 16.
+                            Non-default forms other than 5 / 7 run the general
+                            arithmetic.  Other values: INVALID_ARG. */
 } ntt_opts_t;
 
 /* Prime families for ntt_find_primes_ex. */
@@ -123,13 +138,15 @@ ntt_status_t ntt_plan_info(ntt_plan_t plan, unsigned *L, unsigned *logn, unsigne
                            uint64_t *table_bytes);
 
 /* ntt_plan_exec -- host query of how the plan executes (any output may be NULL):
- * *proth   = 1 if it runs the Proth-prime arithmetic (every prime = 1 mod 2^32
- *            and proth_arith != -1), else 0;
+ * *arith   = the Shoup arithmetic the kernels run (ntt_opts_t.prime_arith):
+ *            NTT_ARITH_GENERAL or NTT_ARITH_PROTH (every prime = 1 mod 2^32);
  * *passes  = kernels per direction (1: single CTA or single-pass cluster
  *            kernel; 2: the paper's two-kernel split);
  * *cluster = CTAs per row of the single-pass cluster kernel (N / 2^13), 1 if
  *            it is not used. */
-ntt_status_t ntt_plan_exec(ntt_plan_t plan, int *proth, unsigned *passes, unsigned *cluster);
+#define NTT_ARITH_GENERAL 0
+#define NTT_ARITH_PROTH 1
+ntt_status_t ntt_plan_exec(ntt_plan_t plan, int *arith, unsigned *passes, unsigned *cluster);
 
 /* ntt_forward -- in-place forward merged negacyclic NTT of batch*L rows.
  *   data: DEVICE pointer on the plan's device, 16-byte aligned, to
@@ -182,34 +199,48 @@ ntt_status_t ntt_pointwise_inverse(ntt_plan_t plan, const uint64_t *a_ntt, uint6
 ntt_status_t ntt_negacyclic_mul(ntt_plan_t plan, uint64_t *a, uint64_t *b, unsigned batch, void *stream);
 
 /* ntt_forward_variant -- the forward transform through one of the paper's
- * comparison implementations, rebuilt for sm_100a, for
- * the paper's radix-2 vs SMEM ratio (Table 2):
+ * comparison implementations, rebuilt for sm_100a:
  *   NTT_VARIANT_DEFAULT  (0): the two-kernel SMEM path (== ntt_forward);
  *   NTT_VARIANT_RADIX2   (1): Algorithm 1, one launch per stage, every
  *                             butterfly through global memory;
+ *                             the paper's radix-2 vs SMEM ratio (Table 2
+ *                             P:850-866);
  *   NTT_VARIANT_RADIX16  (2): register-based radix-16 passes, no shared
- *                             memory, ceil(log2 N / 4) launches.
+ *                             memory, ceil(log2 N / 4) launches;
+ *   NTT_VARIANT_NATIVE   (3): the default kernels (same split, same schedule)
+ *                             with every twiddle product reduced by the native
+ *                             modulo operation, (unsigned __int128)(b w) % p,
+ *                             instead of Shoup's modmul -- the paper's "Native"
+ *                             arm of fig:native_shoup ((2^17, 45)).
+ *                             No OT, not for plans with the cluster kernel.
  * Output identical to ntt_forward (bit-exact).  Same data contract and errors,
- * plus INVALID_ARG for an unknown variant. */
+ * plus INVALID_ARG for an unknown variant (or NATIVE on a fused / OT plan). */
 #define NTT_VARIANT_DEFAULT 0u
 #define NTT_VARIANT_RADIX2 1u
 #define NTT_VARIANT_RADIX16 2u
+#define NTT_VARIANT_NATIVE 3u
 ntt_status_t ntt_forward_variant(ntt_plan_t plan, uint64_t *data, unsigned batch, unsigned variant, void *stream);
 
 /* ntt_execute_host -- the end-to-end path with HOST buffers: for each chunk of
  * ciphertexts, copy host_in -> device workspace, run the requested transforms
  * (flags: NTT_DIR_FORWARD, NTT_DIR_INVERSE, or both = forward then inverse),
- * copy back to host_out (may equal host_in).  Chunks are pipelined over two
- * internal streams so H2D, kernels and D2H overlap.
+ * copy back to host_out (may equal host_in).  Chunks are pipelined over three
+ * internal streams (pipeline slots) so chunk k's H2D, chunk k-1's kernels and
+ * chunk k-2's D2H overlap.
  *   host_in/host_out: HOST pointers to batch x L x N words (pinned memory gives
  *   overlap; pageable memory works but serialises).
  *   workspace: DEVICE pointer on the plan's device, 16-byte aligned, of at
  *   least ntt_workspace_words(plan, chunk) words; chunk = ciphertexts per
  *   pipeline step (0 = automatic).
+ *   stream: cudaStream_t (as void*, NULL = legacy default stream) the
+ *   workspace is ordered on: the internal streams wait for the work already
+ *   queued on it before touching the workspace (e.g. a stream-ordered
+ *   allocation that is still in use).
  *   Synchronous: returns when host_out holds the result.
  *   Errors: as ntt_forward, plus INVALID_ARG for a too-small workspace. */
 ntt_status_t ntt_execute_host(ntt_plan_t plan, unsigned flags, const uint64_t *host_in, uint64_t *host_out,
-                              unsigned batch, uint64_t *workspace, uint64_t workspace_words, unsigned chunk);
+                              unsigned batch, uint64_t *workspace, uint64_t workspace_words, unsigned chunk,
+                              void *stream);
 
 /* Words of device workspace ntt_execute_host needs for a given chunk (0 = auto). */
 uint64_t ntt_workspace_words(ntt_plan_t plan, unsigned batch, unsigned chunk);
@@ -217,6 +248,67 @@ uint64_t ntt_workspace_words(ntt_plan_t plan, unsigned batch, unsigned chunk);
 /* ntt_plan_destroy -- frees the plan's device tables and host state.
  * NULL is accepted (no-op).  Caller must have synchronised all work. */
 ntt_status_t ntt_plan_destroy(ntt_plan_t plan);
+
+/* ---------------------------------------------------------------- request graphs
+ * Small requests (one ciphertext of a few primes, BASELINE config 5) are bound
+ * by host launch cost, not by the kernels.  A request graph is
+ * the CUDA graph of one fixed call -- the kernels of the forward and / or
+ * inverse transform of `batch` ciphertexts at a fixed device buffer --
+ * captured once and replayed with one cudaGraphLaunch per request: the caller
+ * copies each request into the buffer (or produces it there) and launches.
+ *
+ * ntt_graph_create -- capture the transforms `flags` (NTT_DIR_FORWARD,
+ * NTT_DIR_INVERSE, or both = forward then inverse; NTT_GRAPH_PRODUCT = the
+ * negacyclic product b <- a * b of ntt_negacyclic_mul with a = data and
+ * b = data2) of plan over data[0 .. batch*L*N) into *graph.  data / data2:
+ * DEVICE pointers as for ntt_forward; they are baked into the graph and must
+ * stay valid while it exists.  The graph holds a reference to the plan's
+ * tables: destroy the graph before the plan.  Synchronous; enqueues nothing.
+ * Errors: as ntt_forward, INVALID_ARG (graph NULL, flags 0 or unknown,
+ * batch 0, data2 NULL with NTT_GRAPH_PRODUCT), CUDA (capture failed). */
+typedef struct ntt_graph_s *ntt_graph_t;
+#define NTT_GRAPH_PRODUCT 4u
+ntt_status_t ntt_graph_create(ntt_graph_t *graph, ntt_plan_t plan, uint64_t *data, uint64_t *data2, unsigned batch,
+                              unsigned flags);
+
+/* ntt_graph_launch -- enqueue one replay of the graph on `stream`
+ * (cudaStream_t as void*, NULL = legacy default).  Asynchronous, ordered
+ * after earlier work on `stream`.  A graph must not be replayed concurrently
+ * with itself on two streams (its buffer is shared).  Errors: INVALID_ARG
+ * (graph NULL), CUDA. */
+ntt_status_t ntt_graph_launch(ntt_graph_t graph, void *stream);
+
+/* ntt_graph_destroy -- frees the graph; NULL accepted.  Replays must be done. */
+ntt_status_t ntt_graph_destroy(ntt_graph_t graph);
+
+/* ---------------------------------------------------------------- host helpers for tests
+ * ntt_shoup_companion -- *wb = floor(w 2^64 / p), the Shoup companion of w
+ * (Algorithm 4 precompute; R6) exactly as the plan tables store it.
+ * Host only.  Errors: INVALID_ARG (wb NULL, p < 2, w >= p). */
+ntt_status_t ntt_shoup_companion(uint64_t w, uint64_t p, uint64_t *wb);
+
+/* ntt_table_sizes -- the twiddle storage a plan with (n, L, OT base) holds,
+ * from the same function plan creation sizes its allocations with.  Host only.
+ *   *psi_bytes  = bytes of one direction's bit-reversed tables, L x N
+ *                 (w, w_bar) pairs ("2 N np words" doubled by w_bar);
+ *   *ot_entries = (w, w_bar) pairs of one prime's OT base tables,
+ *                 B + N / B;
+ *   *plan_bytes = all device bytes of a default (two-kernel) plan.
+ * Any output may be NULL.  ot_base 0 = the default of ntt_opts_t.
+ * Errors: INVALID_N, INVALID_ARG (L == 0, bad base). */
+ntt_status_t ntt_table_sizes(unsigned n, unsigned L, unsigned ot_base, uint64_t *psi_bytes, uint64_t *ot_entries,
+                             uint64_t *plan_bytes);
+
+/* ntt_debug_corrupt_twiddle -- TESTING ONLY (fault injection for the parity
+ * harness): XOR `mask` into the twiddle w (field 0) or its Shoup companion
+ * w_bar (field 1) of Psi[index] (dir NTT_DIR_FORWARD) or Psi^-1[index]
+ * (NTT_DIR_INVERSE) of prime l, in every device copy of the plan's
+ * bit-reversed tables (the standard and the Kernel-2-ordered one; the OT base
+ * tables are not touched).  XOR-ing the same mask again restores the plan.
+ * Synchronous (device-wide).  Errors: INVALID_ARG (bad dir / l / index /
+ * field), CUDA. */
+ntt_status_t ntt_debug_corrupt_twiddle(ntt_plan_t plan, unsigned dir, unsigned l, unsigned index, unsigned field,
+                                       uint64_t mask);
 
 /* ---------------------------------------------------------------- 32-bit words
  * The paper's 32-bit-word alternative ("32b vs 64b"; SURVEY 8(f)

@@ -14,10 +14,11 @@ from __future__ import annotations
 
 import ctypes
 
-from ._native import NTT_DIR_FORWARD, NTT_DIR_INVERSE, NTT_PRIMES_2N, NTT_PRIMES_PROTH32, NttError, Opts, check, lib
+from ._native import (NTT_ARITH_PROTH, NTT_DIR_FORWARD, NTT_DIR_INVERSE, NTT_GRAPH_PRODUCT, NTT_PRIMES_2N,
+                      NTT_PRIMES_PROTH32, NttError, Opts, check, lib)
 
-__all__ = ["Plan", "Plan32", "find_primes", "find_primes32", "find_psi", "NttError", "NTT_DIR_FORWARD",
-           "NTT_DIR_INVERSE"]
+__all__ = ["Plan", "Plan32", "Graph", "find_primes", "find_primes32", "find_psi", "table_sizes", "shoup_companion",
+           "NttError", "NTT_DIR_FORWARD", "NTT_DIR_INVERSE", "NTT_GRAPH_PRODUCT"]
 
 
 PRIME_FORMS = {"2n": NTT_PRIMES_2N, "proth": NTT_PRIMES_PROTH32}
@@ -43,6 +44,45 @@ def find_psi(p: int, N: int) -> int:
     v = ctypes.c_uint64()
     check(lib().ntt_find_psi(p, N, ctypes.byref(v)), "ntt_find_psi")
     return int(v.value)
+
+
+def shoup_companion(w: int, p: int) -> int:
+    """floor(w 2^64 / p), as the plan tables store it (host, R6)."""
+    v = ctypes.c_uint64()
+    check(lib().ntt_shoup_companion(w, p, ctypes.byref(v)), "ntt_shoup_companion")
+    return int(v.value)
+
+
+def table_sizes(N: int, L: int, ot_base: int = 0) -> dict:
+    """Twiddle storage of a plan (host): bytes of one direction's Psi tables,
+    OT base entries per prime, and all device bytes of a default plan."""
+    a, b, c = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    check(lib().ntt_table_sizes(N, L, ot_base, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), "ntt_table_sizes")
+    return {"psi_bytes": int(a.value), "ot_entries": int(b.value), "plan_bytes": int(c.value)}
+
+
+def _host_ptr(a, what: str) -> tuple[int, int]:
+    """(address, 64-bit words) of a C-contiguous CPU buffer of 64-bit integers
+    (numpy array or CPU torch tensor)."""
+    import numpy as np
+
+    if hasattr(a, "data_ptr"):  # torch
+        import torch
+
+        if a.device.type != "cpu":
+            raise ValueError(f"{what} must be a CPU (host) tensor")
+        if a.dtype not in (torch.int64, torch.uint64):
+            raise TypeError(f"{what} must hold 64-bit integers, got {a.dtype}")
+        if not a.is_contiguous():
+            raise ValueError(f"{what} must be contiguous")
+        return a.data_ptr(), a.numel()
+    if not isinstance(a, np.ndarray):
+        raise TypeError(f"{what} must be a numpy array or a CPU torch tensor")
+    if a.dtype not in (np.uint64, np.int64):
+        raise TypeError(f"{what} must hold 64-bit integers, got {a.dtype}")
+    if not a.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"{what} must be C-contiguous")
+    return a.ctypes.data, a.size
 
 
 def _dev_ptr(t, N: int, L: int, bits: int = 64) -> tuple[int, int]:
@@ -82,13 +122,14 @@ class Plan:
     CUDA device (ntt_plan_create_ex)."""
 
     def __init__(self, N: int, primes, ot: bool = False, ot_base: int = 0, ot_stages: int = 0,
-                 log_n1: int = 0, proth_arith: bool = True, fused: bool | None = None):
+                 log_n1: int = 0, proth_arith: bool = True, fused: bool | None = None,
+                 k1_variant: int = 0, k2_variant: int = 0):
         self.N = int(N)
         self.primes = [int(p) for p in primes]
         self.L = len(self.primes)
         arr = (ctypes.c_uint64 * max(self.L, 1))(*self.primes)
         opts = Opts(1 if ot else -1, ot_base, ot_stages, log_n1, 0 if proth_arith else -1,
-                    0 if fused is None else (1 if fused else -1))
+                    0 if fused is None else (1 if fused else -1), k1_variant, k2_variant)
         h = ctypes.c_void_p()
         check(lib().ntt_plan_create_ex(ctypes.byref(h), self.N, arr, self.L, ctypes.byref(opts)),
               "ntt_plan_create")
@@ -116,7 +157,8 @@ class Plan:
         npass, ncl = ctypes.c_uint(), ctypes.c_uint()
         check(lib().ntt_plan_exec(self.handle, ctypes.byref(pr), ctypes.byref(npass), ctypes.byref(ncl)))
         return {"L": L.value, "logn": logn.value, "log_n1": logn1.value, "ot_enable": bool(ote.value),
-                "ot_base": otb.value, "ot_stages": ots.value, "table_bytes": tb.value, "proth": bool(pr.value),
+                "ot_base": otb.value, "ot_stages": ots.value, "table_bytes": tb.value,
+                "proth": pr.value == NTT_ARITH_PROTH, "arith": "proth" if pr.value == NTT_ARITH_PROTH else "general",
                 "passes": npass.value, "cluster": ncl.value}
 
     # ---------------------------------------------------------------- transforms
@@ -165,7 +207,8 @@ class Plan:
 
     def forward_variant(self, x, variant: int, stream=None):
         """Forward NTT through one of the paper's comparison kernels
-        (1 = radix-2 per stage, 2 = register radix-16; 0 = default path)."""
+        (1 = radix-2 per stage, 2 = register radix-16, 3 = default kernels with
+        native-modulo twiddle products; 0 = default path)."""
         ptr, batch = _dev_ptr(x, self.N, self.L)
         check(lib().ntt_forward_variant(self.handle, ptr, batch, variant, _stream_handle(stream, x)),
               "ntt_forward_variant")
@@ -174,25 +217,76 @@ class Plan:
     def workspace_words(self, batch: int, chunk: int = 0) -> int:
         return int(lib().ntt_workspace_words(self.handle, batch, chunk))
 
-    def execute_host(self, host_in, host_out, flags: int, workspace, chunk: int = 0) -> None:
-        """End-to-end transform of HOST buffers (numpy arrays or CPU tensors,
-        ideally pinned) through a device workspace; synchronous."""
-        def hptr(a):
-            if hasattr(a, "data_ptr"):
-                return a.data_ptr(), a.numel()
-            return a.ctypes.data, a.size
-        pin, n_in = hptr(host_in)
-        pout, n_out = hptr(host_out)
+    def execute_host(self, host_in, host_out, flags: int, workspace, chunk: int = 0, stream=None) -> None:
+        """End-to-end transform of HOST buffers (C-contiguous 64-bit numpy
+        arrays or CPU tensors, ideally pinned) through a CUDA workspace tensor
+        of 64-bit words; synchronous.  The workspace is used after the work
+        already queued on `stream` (default: the current stream)."""
+        pin, n_in = _host_ptr(host_in, "host_in")
+        pout, n_out = _host_ptr(host_out, "host_out")
         if n_in != n_out or n_in % (self.N * self.L):
             raise ValueError("host buffers must both hold batch*L*N words")
-        wptr = workspace.data_ptr()
-        check(lib().ntt_execute_host(self.handle, flags, pin, pout, n_in // (self.N * self.L), wptr,
-                                     workspace.numel(), chunk), "ntt_execute_host")
+        batch = n_in // (self.N * self.L)
+        wptr, _ = _dev_ptr(workspace, 1, 1)
+        check(lib().ntt_execute_host(self.handle, flags, pin, pout, batch, wptr, workspace.numel(), chunk,
+                                     _stream_handle(stream, workspace)), "ntt_execute_host")
+
+    def graph(self, x, flags: int = NTT_DIR_FORWARD | NTT_DIR_INVERSE, other=None) -> "Graph":
+        """Capture the transforms `flags` of the CUDA tensor x (or, with
+        NTT_GRAPH_PRODUCT, the product other <- x * other) into a replayable
+        request graph (ntt_graph_create)."""
+        return Graph(self, x, flags, other)
+
+    def corrupt_twiddle(self, direction: int, l: int, index: int, field: int, mask: int) -> None:
+        """TESTING ONLY: XOR mask into Psi[index] (field 0 = w, 1 = w_bar) of
+        prime l in the plan's device tables (ntt_debug_corrupt_twiddle)."""
+        check(lib().ntt_debug_corrupt_twiddle(self.handle, direction, l, index, field, mask),
+              "ntt_debug_corrupt_twiddle")
 
     # ---------------------------------------------------------------- lifetime
     def close(self) -> None:
         if getattr(self, "_h", None) is not None:
             lib().ntt_plan_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Graph:
+    """A captured request (ntt_graph_create): replay with launch(); the tensor(s)
+    it was captured on are baked in and kept alive with the plan."""
+
+    def __init__(self, plan: Plan, x, flags: int, other=None):
+        ptr, batch = _dev_ptr(x, plan.N, plan.L)
+        ptr2 = 0
+        if other is not None:
+            ptr2, b2 = _dev_ptr(other, plan.N, plan.L)
+            if b2 != batch:
+                raise ValueError("operands must have the same batch")
+        h = ctypes.c_void_p()
+        check(lib().ntt_graph_create(ctypes.byref(h), plan.handle, ptr, ptr2 or None, batch, flags),
+              "ntt_graph_create")
+        self._h = h
+        self._keep = (plan, x, other)
+
+    def launch(self, stream=None) -> None:
+        if self._h is None:
+            raise ValueError("graph destroyed")
+        check(lib().ntt_graph_launch(self._h, _stream_handle(stream, self._keep[1])), "ntt_graph_launch")
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None:
+            lib().ntt_graph_destroy(self._h)
             self._h = None
 
     def __enter__(self):

@@ -17,8 +17,10 @@ STATUS = {
 }
 NTT_DIR_FORWARD = 1
 NTT_DIR_INVERSE = 2
-NTT_VARIANT_DEFAULT, NTT_VARIANT_RADIX2, NTT_VARIANT_RADIX16 = 0, 1, 2
+NTT_VARIANT_DEFAULT, NTT_VARIANT_RADIX2, NTT_VARIANT_RADIX16, NTT_VARIANT_NATIVE = 0, 1, 2, 3
 NTT_PRIMES_2N, NTT_PRIMES_PROTH32 = 0, 1
+NTT_ARITH_GENERAL, NTT_ARITH_PROTH = 0, 1
+NTT_GRAPH_PRODUCT = 4
 
 # every symbol include/ntt.h declares
 EXPORTS = [
@@ -26,6 +28,8 @@ EXPORTS = [
     "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_launch_pass", "ntt_pointwise_inverse", "ntt_negacyclic_mul", "ntt_forward_variant",
     "ntt_execute_host", "ntt_workspace_words",
     "ntt_plan_destroy", "ntt_status_string",
+    "ntt_graph_create", "ntt_graph_launch", "ntt_graph_destroy",
+    "ntt_shoup_companion", "ntt_table_sizes", "ntt_debug_corrupt_twiddle",
     "ntt_find_primes32", "ntt_plan_create32", "ntt_plan_info32", "ntt_forward32", "ntt_inverse32",
     "ntt_plan_destroy32",
 ]
@@ -41,8 +45,8 @@ class NttError(RuntimeError):
 
 class Opts(ctypes.Structure):
     _fields_ = [("ot_enable", ctypes.c_int), ("ot_base", ctypes.c_uint),
-                ("ot_stages", ctypes.c_uint), ("log_n1", ctypes.c_uint), ("proth_arith", ctypes.c_int),
-                ("fused", ctypes.c_int)]
+                ("ot_stages", ctypes.c_uint), ("log_n1", ctypes.c_uint), ("prime_arith", ctypes.c_int),
+                ("fused", ctypes.c_int), ("k1_variant", ctypes.c_int), ("k2_variant", ctypes.c_int)]
 
 
 _lib = None
@@ -73,7 +77,13 @@ def lib() -> ctypes.CDLL:
         L.ntt_forward_variant.argtypes = [vp, vp, u32, u32, vp]
         L.ntt_pointwise_inverse.argtypes = [vp, vp, vp, u32, vp]
         L.ntt_negacyclic_mul.argtypes = [vp, vp, vp, u32, vp]
-        L.ntt_execute_host.argtypes = [vp, u32, vp, vp, u32, vp, u64, u32]
+        L.ntt_execute_host.argtypes = [vp, u32, vp, vp, u32, vp, u64, u32, vp]
+        L.ntt_graph_create.argtypes = [pp, vp, vp, vp, u32, u32]
+        L.ntt_graph_launch.argtypes = [vp, vp]
+        L.ntt_graph_destroy.argtypes = [vp]
+        L.ntt_shoup_companion.argtypes = [u64, u64, p64]
+        L.ntt_table_sizes.argtypes = [u32, u32, u32, p64, p64, p64]
+        L.ntt_debug_corrupt_twiddle.argtypes = [vp, u32, u32, u32, u32, u64]
         L.ntt_workspace_words.argtypes = [vp, u32, u32]
         L.ntt_workspace_words.restype = u64
         L.ntt_plan_destroy.argtypes = [vp]
@@ -90,7 +100,9 @@ def lib() -> ctypes.CDLL:
                      "ntt_plan_psi", "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_launch_pass", "ntt_forward_variant",
                      "ntt_pointwise_inverse", "ntt_negacyclic_mul", "ntt_execute_host",
                      "ntt_plan_destroy", "ntt_find_primes32", "ntt_plan_create32", "ntt_plan_info32",
-                     "ntt_forward32", "ntt_inverse32", "ntt_plan_destroy32"]:
+                     "ntt_forward32", "ntt_inverse32", "ntt_plan_destroy32", "ntt_graph_create",
+                     "ntt_graph_launch", "ntt_graph_destroy", "ntt_shoup_companion", "ntt_table_sizes",
+                     "ntt_debug_corrupt_twiddle"]:
             getattr(L, name).restype = i32
         _lib = L
     return _lib

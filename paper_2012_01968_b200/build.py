@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-I", os.path.join(ROOT, "include")]
 
-SOURCES = ["ntt_kernels.cu", "ntt_kernels_p.cu", "ntt_fused.cu", "ntt32.cu", "ntt_baselines.cu", "ntt_api.cu", "ntt32_api.cu", "params.cpp"]
+SOURCES = ["ntt_kernels.cu", "ntt_kernels_p.cu", "ntt_native.cu", "ntt_fused.cu", "ntt32.cu", "ntt_baselines.cu", "ntt_api.cu", "ntt32_api.cu", "params.cpp"]
 HEADERS = ["ntt_kernels.cuh", "ntt_fused.cuh", "ntt_device.cuh", "ntt_launch.h", "params.h"]
 
 
@@ -55,5 +55,18 @@ def build(force: bool = False) -> str:
     return LIB
 
 
+def build_ceiling_probe(force: bool = False) -> str:
+    """tools/libs/bf_roof: the register-only butterfly throughput probe (the
+    practical ALU ceiling bench.py reports its roofline against)."""
+    src = os.path.join(ROOT, "tools", "bf_roof.cu")
+    out = os.path.join(ROOT, "tools", "libs", "bf_roof")
+    deps = [src, os.path.join(CSRC, "ntt_device.cuh")]
+    if force or _newer(out, deps):
+        os.makedirs(os.path.dirname(out), exist_ok=True)
+        subprocess.check_call([NVCC, *ARCH, "-O3", "-std=c++17", "-I", os.path.join(ROOT, "include"), "-o", out, src])
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv))
+    print(build_ceiling_probe(force="--force" in sys.argv))

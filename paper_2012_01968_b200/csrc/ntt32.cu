@@ -424,24 +424,19 @@ __global__ void __launch_bounds__(Contig32Cfg<LOGM>::CT,
 
 // ------------------------------------------------------------ dispatch
 namespace {
-bool set_once32(std::atomic<uint64_t>& mask)
-{
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const uint64_t bit = 1ull << (dev & 63);
-    return mask.fetch_or(bit) & bit;
-}
-
 template <int LOGN1, int LOGN, bool INV>
 cudaError_t launch32_cols_t(const KArgs32& a, uint32_t rows, cudaStream_t st)
 {
     constexpr int M = 1 << LOGN1, CT = (M / 16) * 32;
     const size_t smem = (size_t)M * 32 * 4 + (size_t)M * sizeof(Tw32);
     auto fn = w32::k32_cols<LOGN1, LOGN, INV>;
-    static std::atomic<uint64_t> attr{0};
-    if (!set_once32(attr)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static DeviceOnce once;
+    if (cudaError_t e = once.run([&](int&) {
+            return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        }))
+        return e;
     fn<<<(unsigned)((uint64_t)rows << a.log_tiles), CT, smem, st>>>(a);
-    return cudaPeekAtLastError();
+    return launch_status();
 }
 
 template <int LOGM, bool INV, bool FUSE0, bool K2, bool SHARED>
@@ -451,12 +446,15 @@ cudaError_t launch32_contig_t(const KArgs32& a, cudaStream_t st)
     const size_t smem = (size_t)CC::NB * (1 << LOGM) * 4 + (SHARED ? sizeof(Tw32) << LOGM : 0);
     // Kernel-2 runs the remainder-last schedule (the plan's Kernel-2 table follows it)
     auto fn = w32::k32_contig<LOGM, INV, FUSE0, K2, SHARED, K2 ? (4 | kRemLast) : 4>;
-    static std::atomic<uint64_t> attr{0};
-    if (!set_once32(attr)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static DeviceOnce once;
+    if (cudaError_t e = once.run([&](int&) {
+            return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        }))
+        return e;
     const uint32_t grid = SHARED ? (a.L << a.log_n1) * ((a.batch + CC::NB - 1) / CC::NB)
                                  : (a.total_blocks + CC::NB - 1) / CC::NB;
     fn<<<grid, CC::CT, smem, st>>>(a);
-    return cudaPeekAtLastError();
+    return launch_status();
 }
 
 template <bool INV, bool FUSE0, bool K2, int... Ls>

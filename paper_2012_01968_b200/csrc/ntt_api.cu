@@ -5,6 +5,7 @@
 #include "params.h"
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -37,7 +38,7 @@ struct ntt_plan_s {
     // CTA per block position on the remainder-last schedule, 7 = the same on the remainder-first schedule,
     // 5 = persistent pipelined, 6 = pipelined radix 8, 3/4 = one-shot radix 8/16)
     int loge_k1 = 4, loge_k2 = 9;
-    bool proth = false;            // every prime = 1 mod 2^32: PrimeConstP kernels
+    int arith = ntt::kArithGeneral;  // prime-constant type of the kernels (ntt_launch.h)
     bool fused = false;            // single-pass cluster kernel per direction (log_n1 = log2 cluster size)
 };
 
@@ -113,6 +114,20 @@ ntt_status_t check_data(const ntt_plan_s* plan, const void* data)
     return NTT_OK;
 }
 
+// Kernel index arithmetic is 32-bit: batch * L * N1 (rows times column tiles
+// or block positions) must stay below 2^31 on every entry point that enqueues.
+ntt_status_t check_batch(const ntt_plan_s* plan, uint64_t batch)
+{
+    return (batch * plan->L << plan->log_n1) < (1ull << 31) ? NTT_OK : NTT_ERR_INVALID_ARG;
+}
+
+// NVTX range around one C-ABI call (visible under nsys / ncu --nvtx; a no-op
+// without a tool attached).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 KArgs base_args(const ntt_plan_s* plan, uint64_t* data, unsigned batch, bool inverse)
 {
     KArgs a{};
@@ -137,24 +152,24 @@ cudaError_t two_pass(const ntt_plan_s* plan, KArgs a, uint32_t rows, bool invers
     a.log_tiles = plan->logn - plan->log_n1 - 4;
     cudaError_t e = cudaSuccess;
     if (!inverse) {
-        if (pass != 1 && (e = ntt::launch_k1(false, plan->loge_k1, a, rows, st, plan->proth)) != cudaSuccess)
+        if (pass != 1 && (e = ntt::launch_k1(false, plan->loge_k1, a, rows, st, plan->arith)) != cudaSuccess)
             return e;
-        if (pass != 0) e = ntt::launch_k2(false, plan->loge_k2, a, ots, 1, st, plan->proth);
+        if (pass != 0) e = ntt::launch_k2(false, plan->loge_k2, a, ots, 1, st, plan->arith);
         return e;
     }
     if (pass != 1) {
-        e = ntt::launch_k2(true, plan->loge_k2, a, ots, 1, st, plan->proth);
+        e = ntt::launch_k2(true, plan->loge_k2, a, ots, 1, st, plan->arith);
         if (e == cudaErrorNotSupported && a.mul_a) {  // unfused: product kernel, then Kernel-2'
             cudaGetLastError();
             if ((e = ntt::launch_pointwise(a, st)) != cudaSuccess) return e;
             KArgs b = a;
             b.mul_a = nullptr;
-            e = ntt::launch_k2(true, plan->loge_k2, b, ots, 1, st, plan->proth);
+            e = ntt::launch_k2(true, plan->loge_k2, b, ots, 1, st, plan->arith);
         }
         if (e != cudaSuccess) return e;
     }
     a.mul_a = nullptr;
-    if (pass != 0) e = ntt::launch_k1(true, plan->loge_k1, a, rows, st, plan->proth);
+    if (pass != 0) e = ntt::launch_k1(true, plan->loge_k1, a, rows, st, plan->arith);
     return e;
 }
 
@@ -177,16 +192,16 @@ cudaError_t enqueue(const ntt_plan_s* plan, uint64_t* data, unsigned batch, bool
             if (e != cudaSuccess) return e;
             a.mul_a = nullptr;
         }
-        return ntt::launch_fused(inverse, a, rows, st, plan->proth);
+        return ntt::launch_fused(inverse, a, rows, st, plan->arith);
     }
     if (plan->log_n1 == 0) {
         a.total_blocks = rows;
-        cudaError_t e = ntt::launch_single(inverse, a, ots, 1, st, plan->proth);
+        cudaError_t e = ntt::launch_single(inverse, a, ots, 1, st, plan->arith);
         if (e == cudaErrorNotSupported && mul_a) {  // unfused: product kernel, then the inverse
             cudaGetLastError();
             if ((e = ntt::launch_pointwise(a, st)) != cudaSuccess) return e;
             a.mul_a = nullptr;
-            e = ntt::launch_single(inverse, a, ots, 1, st, plan->proth);
+            e = ntt::launch_single(inverse, a, ots, 1, st, plan->arith);
         }
         return e;
     }
@@ -198,11 +213,32 @@ ntt_status_t run(ntt_plan_t plan, uint64_t* data, unsigned batch, void* stream, 
     if (!plan || !data) return NTT_ERR_INVALID_ARG;
     if (batch == 0) return NTT_OK;
     ntt_status_t s = check_data(plan, data);
+    if (s == NTT_OK) s = check_batch(plan, batch);
     if (s != NTT_OK) return s;
-    if ((uint64_t)batch * plan->L * ((uint64_t)1 << plan->log_n1) >= (1ull << 31)) return NTT_ERR_INVALID_ARG;
     DeviceGuard g(plan->device);
     return enqueue(plan, data, batch, inverse, (cudaStream_t)stream, pass) == cudaSuccess ? NTT_OK : NTT_ERR_CUDA;
 }
+
+// Device bytes of a plan's twiddle storage (ntt_table_sizes and plan creation):
+// per direction L x N Shoup pairs (doubled by w_bar), their Kernel-2
+// ordered copies for the two-kernel / cluster paths, the OT bases
+// (B + N/B pairs per prime and direction), and two PrimeConst
+// arrays (plain and R-scaled N^-1).
+struct TableSizes {
+    uint64_t psi_dir, ot_per_prime, ot_dir, pc, total;
+};
+TableSizes table_sizes(uint64_t N, unsigned L, uint64_t ot_base, bool k2tab)
+{
+    TableSizes t;
+    t.psi_dir = sizeof(Tw) * N * L;
+    t.ot_per_prime = ot_base + N / ot_base;
+    t.ot_dir = sizeof(Tw) * t.ot_per_prime * L;
+    t.pc = sizeof(PrimeConst) * L;
+    t.total = (k2tab ? 4 : 2) * t.psi_dir + 2 * t.ot_dir + 2 * t.pc;
+    return t;
+}
+
+unsigned default_ot_base(unsigned logn) { return logn >= 11 ? 1024u : (1u << ((logn + 1) / 2)); }
 
 }  // namespace
 
@@ -292,20 +328,31 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
     if (opts.ot_enable < -1 || opts.ot_enable > 1) return NTT_ERR_INVALID_ARG;
     const int ot_enable = opts.ot_enable == 1;
     unsigned ot_base = opts.ot_base;
-    if (ot_base == 0) ot_base = logn >= 11 ? 1024u : (1u << ((logn + 1) / 2));
+    if (ot_base == 0) ot_base = default_ot_base(logn);
     if ((ot_base & (ot_base - 1)) || ot_base > n) return NTT_ERR_INVALID_ARG;
     unsigned ot_stages = opts.ot_stages ? opts.ot_stages : 2;
     if (ot_stages > 2) return NTT_ERR_INVALID_ARG;
     const unsigned last_kernel_stages = log_n1 ? logn - log_n1 : logn;
     if (ot_stages > last_kernel_stages) ot_stages = last_kernel_stages;
-    if (opts.proth_arith < -1 || opts.proth_arith > 0) return NTT_ERR_INVALID_ARG;
+    if (opts.prime_arith < -1 || opts.prime_arith > 0) return NTT_ERR_INVALID_ARG;
+    // kernel variants (tuning and experiments): 0 = default
+    int loge_k1 = 4, loge_k2 = 9;
+    if (opts.k1_variant) {
+        if (opts.k1_variant != 4 && opts.k1_variant != 5) return NTT_ERR_INVALID_ARG;
+        loge_k1 = opts.k1_variant;
+    }
+    if (opts.k2_variant) {
+        if (opts.k2_variant < 3 || opts.k2_variant > 9 || opts.k2_variant == 8) return NTT_ERR_INVALID_ARG;
+        loge_k2 = opts.k2_variant;
+    }
     if (opts.fused < -1 || opts.fused > 1) return NTT_ERR_INVALID_ARG;
     // single pass per direction (cluster kernel): N = 2^14..2^17, no OT, no explicit split
     const bool fused_ok = logn >= 14 && logn <= 17 && !ot_enable && opts.log_n1 == 0;
     if (opts.fused == 1 && !fused_ok) return NTT_ERR_INVALID_ARG;
     const bool fused = fused_ok && opts.fused == 1;
     if (fused) log_n1 = logn - 13;
-    bool all_proth = opts.proth_arith == 0;
+    // Proth arithmetic when every prime has the form
+    bool all_proth = opts.prime_arith == 0;
     for (unsigned i = 0; i < L; ++i) all_proth = all_proth && (uint32_t)pr[i] == 1u;
 
     int dev = 0;
@@ -331,16 +378,11 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
     p->ot_stages = ot_stages;
     p->primes = pr;
     p->psis.assign(L, 0);
-    // tuning knob (experiments only): NTT_LOGE="k1,k2" per-thread radix exponents
-    if (const char* v = std::getenv("NTT_LOGE")) {
-        int a1 = 4, a2 = 9;
-        if (std::sscanf(v, "%d,%d", &a1, &a2) == 2 && (a1 >= 3 && a1 <= 5) && (a2 >= 3 && a2 <= 9 && a2 != 8)) {
-            p->loge_k1 = a1;
-            p->loge_k2 = a2;
-        }
-    }
+    p->loge_k1 = loge_k1;
+    p->loge_k2 = loge_k2;
     // the Proth kernels exist for the default variants only (ntt_kernels.cuh)
-    p->proth = all_proth && (((p->loge_k1 == 4 || p->loge_k1 == 5) && (p->loge_k2 == 5 || p->loge_k2 == 7 || p->loge_k2 == 9)) || fused);
+    const bool special_ok = ((loge_k1 == 4 || loge_k1 == 5) && (loge_k2 == 5 || loge_k2 == 7 || loge_k2 == 9)) || fused;
+    p->arith = special_ok && all_proth ? ntt::kArithProth : ntt::kArithGeneral;
     p->fused = fused;
 
     // host tables, one thread per hardware thread over primes
@@ -413,7 +455,8 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
         for (auto& t : th2) t.join();
     }
 
-    const size_t bt = sizeof(Tw) * N * L, bo = sizeof(Tw) * NOT * L, bp = sizeof(PrimeConst) * L;
+    const TableSizes ts = table_sizes(N, L, ot_base, k2tab);
+    const size_t bt = ts.psi_dir, bo = ts.ot_dir, bp = ts.pc;
     if (cudaMalloc(&p->d_fwd, bt) != cudaSuccess || cudaMalloc(&p->d_inv, bt) != cudaSuccess ||
         cudaMalloc(&p->d_ot_fwd, bo) != cudaSuccess || cudaMalloc(&p->d_ot_inv, bo) != cudaSuccess ||
         cudaMalloc(&p->d_pc, bp) != cudaSuccess || cudaMalloc(&p->d_pc_mont, bp) != cudaSuccess ||
@@ -436,7 +479,7 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
         delete p;
         return NTT_ERR_CUDA;
     }
-    p->table_bytes = (k2tab ? 4 : 2) * bt + 2 * bo + bp;
+    p->table_bytes = ts.total;
     *out = p;
     return NTT_OK;
 }
@@ -462,10 +505,10 @@ ntt_status_t ntt_plan_info(ntt_plan_t plan, unsigned* L, unsigned* logn, unsigne
     return NTT_OK;
 }
 
-ntt_status_t ntt_plan_exec(ntt_plan_t plan, int* proth, unsigned* passes, unsigned* cluster)
+ntt_status_t ntt_plan_exec(ntt_plan_t plan, int* arith, unsigned* passes, unsigned* cluster)
 {
     if (!plan) return NTT_ERR_INVALID_ARG;
-    if (proth) *proth = plan->proth ? 1 : 0;
+    if (arith) *arith = plan->arith;
     if (passes) *passes = (plan->fused || plan->log_n1 == 0) ? 1u : 2u;
     if (cluster) *cluster = plan->fused ? (1u << plan->log_n1) : 1u;
     return NTT_OK;
@@ -473,11 +516,13 @@ ntt_status_t ntt_plan_exec(ntt_plan_t plan, int* proth, unsigned* passes, unsign
 
 ntt_status_t ntt_forward(ntt_plan_t plan, uint64_t* data, unsigned batch, void* stream)
 {
+    NvtxRange r("ntt_forward");
     return run(plan, data, batch, stream, false);
 }
 
 ntt_status_t ntt_inverse(ntt_plan_t plan, uint64_t* data, unsigned batch, void* stream)
 {
+    NvtxRange r("ntt_inverse");
     return run(plan, data, batch, stream, true);
 }
 
@@ -493,10 +538,12 @@ ntt_status_t ntt_launch_pass(ntt_plan_t plan, uint64_t* data, unsigned batch, un
 ntt_status_t ntt_pointwise_inverse(ntt_plan_t plan, const uint64_t* a_ntt, uint64_t* data, unsigned batch,
                                    void* stream)
 {
+    NvtxRange r("ntt_pointwise_inverse");
     if (!plan || !data || !a_ntt) return NTT_ERR_INVALID_ARG;
     if (batch == 0) return NTT_OK;
     ntt_status_t s = check_data(plan, data);
     if (s == NTT_OK) s = check_data(plan, a_ntt);
+    if (s == NTT_OK) s = check_batch(plan, batch);
     if (s != NTT_OK) return s;
     DeviceGuard g(plan->device);
     return enqueue(plan, data, batch, true, (cudaStream_t)stream, -1, a_ntt) == cudaSuccess ? NTT_OK : NTT_ERR_CUDA;
@@ -504,6 +551,7 @@ ntt_status_t ntt_pointwise_inverse(ntt_plan_t plan, const uint64_t* a_ntt, uint6
 
 ntt_status_t ntt_negacyclic_mul(ntt_plan_t plan, uint64_t* a, uint64_t* b, unsigned batch, void* stream)
 {
+    NvtxRange r("ntt_negacyclic_mul");
     if (!plan || !a || !b) return NTT_ERR_INVALID_ARG;
     if (a == b) return NTT_ERR_INVALID_ARG;
     ntt_status_t s;
@@ -515,13 +563,23 @@ ntt_status_t ntt_negacyclic_mul(ntt_plan_t plan, uint64_t* a, uint64_t* b, unsig
 ntt_status_t ntt_forward_variant(ntt_plan_t plan, uint64_t* data, unsigned batch, unsigned variant, void* stream)
 {
     if (variant == NTT_VARIANT_DEFAULT) return ntt_forward(plan, data, batch, stream);
-    if (!plan || !data || variant > NTT_VARIANT_RADIX16) return NTT_ERR_INVALID_ARG;
+    NvtxRange r("ntt_forward_variant");
+    if (!plan || !data || variant > NTT_VARIANT_NATIVE) return NTT_ERR_INVALID_ARG;
+    if (variant == NTT_VARIANT_NATIVE && (plan->fused || plan->ot_enable)) return NTT_ERR_INVALID_ARG;
     if (batch == 0) return NTT_OK;
     ntt_status_t s = check_data(plan, data);
+    if (s == NTT_OK) s = check_batch(plan, batch);
     if (s != NTT_OK) return s;
     DeviceGuard g(plan->device);
     const KArgs a = base_args(plan, data, batch, false);
-    return ntt::launch_baseline_forward((int)variant, a, (cudaStream_t)stream) == cudaSuccess ? NTT_OK : NTT_ERR_CUDA;
+    cudaError_t e;
+    if (variant == NTT_VARIANT_NATIVE) {
+        e = ntt::launch_native_forward(a, batch * plan->L, (cudaStream_t)stream);
+        if (e == cudaErrorNotSupported) return NTT_ERR_INVALID_ARG;  // non-default split
+    } else {
+        e = ntt::launch_baseline_forward((int)variant, a, (cudaStream_t)stream);
+    }
+    return e == cudaSuccess ? NTT_OK : NTT_ERR_CUDA;
 }
 
 // pipeline slots (stream + device buffer) of the host-buffer executor: with
@@ -547,24 +605,32 @@ uint64_t ntt_workspace_words(ntt_plan_t plan, unsigned batch, unsigned chunk)
 }
 
 ntt_status_t ntt_execute_host(ntt_plan_t plan, unsigned flags, const uint64_t* host_in, uint64_t* host_out,
-                              unsigned batch, uint64_t* workspace, uint64_t workspace_words, unsigned chunk)
+                              unsigned batch, uint64_t* workspace, uint64_t workspace_words, unsigned chunk,
+                              void* stream)
 {
+    NvtxRange r("ntt_execute_host");
     if (!plan || !host_in || !host_out || (flags & ~3u)) return NTT_ERR_INVALID_ARG;
     if (batch == 0) return NTT_OK;
     ntt_status_t s = check_data(plan, workspace);
     if (s != NTT_OK) return s;
     const unsigned c = auto_chunk(plan, batch, chunk);
+    if ((s = check_batch(plan, c)) != NTT_OK) return s;
     if (workspace_words < ntt_workspace_words(plan, batch, c)) return NTT_ERR_INVALID_ARG;
     DeviceGuard g(plan->device);
     const uint64_t ct_words = (uint64_t)plan->L << plan->logn;
     const unsigned nslot = std::min<unsigned>(kHostSlots, (batch + c - 1) / c);
     cudaStream_t st[kHostSlots] = {};
+    cudaEvent_t ready = nullptr;
     for (unsigned i = 0; i < nslot; ++i)
         if (cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking) != cudaSuccess) {
             for (unsigned j = 0; j < i; ++j) cudaStreamDestroy(st[j]);
+            cudaGetLastError();
             return NTT_ERR_CUDA;
         }
-    cudaError_t e = cudaSuccess;
+    // order the slots after the caller's stream (the workspace may still be in use there)
+    cudaError_t e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(ready, (cudaStream_t)stream);
+    for (unsigned i = 0; i < nslot && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(st[i], ready, 0);
     unsigned k = 0;
     for (unsigned b0 = 0; b0 < batch && e == cudaSuccess; b0 += c, ++k) {
         const unsigned nb = std::min(c, batch - b0);
@@ -577,14 +643,146 @@ ntt_status_t ntt_execute_host(ntt_plan_t plan, unsigned flags, const uint64_t* h
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(host_out + (uint64_t)b0 * ct_words, buf, bytes, cudaMemcpyDeviceToHost, sk);
     }
-    cudaError_t e0 = cudaSuccess, e1 = cudaSuccess;
+    cudaError_t e0 = cudaSuccess;
     for (unsigned i = 0; i < nslot; ++i) {
         const cudaError_t ei = cudaStreamSynchronize(st[i]);
         if (ei != cudaSuccess) e0 = ei;
         cudaStreamDestroy(st[i]);
     }
-    if (e == cudaSuccess) e = e0 != cudaSuccess ? e0 : e1;
+    if (ready) cudaEventDestroy(ready);
+    if (e == cudaSuccess) e = e0;
+    if (e != cudaSuccess) cudaGetLastError();
     return e == cudaSuccess ? NTT_OK : NTT_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------- request graphs
+
+struct ntt_graph_s {
+    int device = 0;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+};
+
+ntt_status_t ntt_graph_create(ntt_graph_t* out, ntt_plan_t plan, uint64_t* data, uint64_t* data2, unsigned batch,
+                              unsigned flags)
+{
+    NvtxRange r("ntt_graph_create");
+    if (!out) return NTT_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (!plan || !data || batch == 0 || flags == 0 || (flags & ~7u)) return NTT_ERR_INVALID_ARG;
+    const bool product = flags & NTT_GRAPH_PRODUCT;
+    if (product && (flags != NTT_GRAPH_PRODUCT || !data2 || data2 == data)) return NTT_ERR_INVALID_ARG;
+    ntt_status_t s = check_data(plan, data);
+    if (s == NTT_OK && product) s = check_data(plan, data2);
+    if (s == NTT_OK) s = check_batch(plan, batch);
+    if (s != NTT_OK) return s;
+    DeviceGuard g(plan->device);
+    ntt_graph_s* gr = new (std::nothrow) ntt_graph_s;
+    if (!gr) return NTT_ERR_OOM;
+    gr->device = plan->device;
+    cudaStream_t st = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        cudaError_t ek = cudaSuccess;
+        if (product) {  // b <- a * b: forward a, forward b, fused odot + inverse (ntt_negacyclic_mul)
+            ek = enqueue(plan, data, batch, false, st);
+            if (ek == cudaSuccess) ek = enqueue(plan, data2, batch, false, st);
+            if (ek == cudaSuccess) ek = enqueue(plan, data2, batch, true, st, -1, data);
+        } else {
+            if (flags & NTT_DIR_FORWARD) ek = enqueue(plan, data, batch, false, st);
+            if (ek == cudaSuccess && (flags & NTT_DIR_INVERSE)) ek = enqueue(plan, data, batch, true, st);
+        }
+        e = cudaStreamEndCapture(st, &gr->graph);  // ends the capture even after a failed launch
+        if (ek != cudaSuccess) e = ek;
+    }
+    if (e == cudaSuccess) e = cudaGraphInstantiateWithFlags(&gr->exec, gr->graph, 0);
+    if (st) cudaStreamDestroy(st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (gr->exec) cudaGraphExecDestroy(gr->exec);
+        if (gr->graph) cudaGraphDestroy(gr->graph);
+        delete gr;
+        return NTT_ERR_CUDA;
+    }
+    *out = gr;
+    return NTT_OK;
+}
+
+ntt_status_t ntt_graph_launch(ntt_graph_t graph, void* stream)
+{
+    if (!graph) return NTT_ERR_INVALID_ARG;
+    if (cudaGraphLaunch(graph->exec, (cudaStream_t)stream) != cudaSuccess) {
+        cudaGetLastError();
+        return NTT_ERR_CUDA;
+    }
+    return NTT_OK;
+}
+
+ntt_status_t ntt_graph_destroy(ntt_graph_t graph)
+{
+    if (!graph) return NTT_OK;
+    {
+        DeviceGuard g(graph->device);
+        if (graph->exec) cudaGraphExecDestroy(graph->exec);
+        if (graph->graph) cudaGraphDestroy(graph->graph);
+    }
+    delete graph;
+    return NTT_OK;
+}
+
+// ---------------------------------------------------------------- host helpers for tests
+
+ntt_status_t ntt_shoup_companion(uint64_t w, uint64_t p, uint64_t* wb)
+{
+    if (!wb || p < 2 || w >= p) return NTT_ERR_INVALID_ARG;
+    *wb = nttp::shoup_pair(w, p).wb;
+    return NTT_OK;
+}
+
+ntt_status_t ntt_table_sizes(unsigned n, unsigned L, unsigned ot_base, uint64_t* psi_bytes, uint64_t* ot_entries,
+                             uint64_t* plan_bytes)
+{
+    if (!pow2_in(n, 1, 17)) return NTT_ERR_INVALID_N;
+    if (L == 0) return NTT_ERR_INVALID_ARG;
+    const unsigned logn = ilog2(n);
+    const unsigned b = ot_base ? ot_base : default_ot_base(logn);
+    if ((b & (b - 1)) || b > n) return NTT_ERR_INVALID_ARG;
+    const TableSizes t = table_sizes(n, L, b, default_log_n1(logn) != 0);
+    if (psi_bytes) *psi_bytes = t.psi_dir;
+    if (ot_entries) *ot_entries = t.ot_per_prime;
+    if (plan_bytes) *plan_bytes = t.total;
+    return NTT_OK;
+}
+
+ntt_status_t ntt_debug_corrupt_twiddle(ntt_plan_t plan, unsigned dir, unsigned l, unsigned index, unsigned field,
+                                       uint64_t mask)
+{
+    if (!plan || (dir != NTT_DIR_FORWARD && dir != NTT_DIR_INVERSE) || l >= plan->L ||
+        index >= (1u << plan->logn) || field > 1)
+        return NTT_ERR_INVALID_ARG;
+    DeviceGuard g(plan->device);
+    const uint64_t N = 1ull << plan->logn;
+    Tw* tab = (dir == NTT_DIR_FORWARD ? plan->d_fwd : plan->d_inv) + l * N;
+    Tw* tab2 = (dir == NTT_DIR_FORWARD ? plan->d_fwd2 : plan->d_inv2);
+    Tw orig;
+    if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpy(&orig, tab + index, sizeof(Tw), cudaMemcpyDeviceToHost))
+        return cudaGetLastError(), NTT_ERR_CUDA;
+    Tw bad = orig;
+    (field ? bad.wb : bad.w) ^= mask;
+    if (cudaMemcpy(tab + index, &bad, sizeof(Tw), cudaMemcpyHostToDevice) != cudaSuccess)
+        return cudaGetLastError(), NTT_ERR_CUDA;
+    if (tab2) {  // the Kernel-2 ordered copy: every Psi entry appears once (entry 0 of a block is padding)
+        std::vector<Tw> h(N);
+        if (cudaMemcpy(h.data(), tab2 + l * N, N * sizeof(Tw), cudaMemcpyDeviceToHost) != cudaSuccess)
+            return cudaGetLastError(), NTT_ERR_CUDA;
+        for (uint64_t i = 0; i < N; ++i)
+            if (h[i].w == orig.w && h[i].wb == orig.wb && (orig.w | orig.wb)) {
+                if (cudaMemcpy(tab2 + l * N + i, &bad, sizeof(Tw), cudaMemcpyHostToDevice) != cudaSuccess)
+                    return cudaGetLastError(), NTT_ERR_CUDA;
+            }
+    }
+    return NTT_OK;
 }
 
 ntt_status_t ntt_plan_destroy(ntt_plan_t plan)

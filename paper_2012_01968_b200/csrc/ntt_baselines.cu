@@ -93,7 +93,7 @@ cudaError_t launch_baseline_forward(int variant, const KArgs& a, cudaStream_t st
                 k_radix2_stage<true><<<grid, 256, 0, st>>>(a, s);
             else
                 k_radix2_stage<false><<<grid, 256, 0, st>>>(a, s);
-            cudaError_t e = cudaPeekAtLastError();
+            cudaError_t e = launch_status();
             if (e != cudaSuccess) return e;
         }
         return cudaSuccess;
@@ -110,7 +110,7 @@ cudaError_t launch_baseline_forward(int variant, const KArgs& a, cudaStream_t st
                 case 2: k_radix_reg<4><<<grid, 256, 0, st>>>(a, S, last); break;
                 default: k_radix_reg<2><<<grid, 256, 0, st>>>(a, S, last); break;
             }
-            cudaError_t e = cudaPeekAtLastError();
+            cudaError_t e = launch_status();
             if (e != cudaSuccess) return e;
             S += r;
         }

@@ -16,7 +16,7 @@ struct __align__(16) Tw {
     uint64_t w, wb;
 };
 
-// Per-prime constants, 64 bytes.
+// Per-prime constants, 112 bytes.
 struct __align__(16) PrimeConst {
     uint64_t p, p2, p4;  // p, 2p, 4p
     uint64_t np;         // 2^64 - p
@@ -38,6 +38,13 @@ struct __align__(16) PrimeConst {
 // Kernels templated on PrimeConstP are launched only for plans whose primes
 // all have this form (ntt_api.cu).
 struct PrimeConstP : PrimeConst {
+};
+
+// The same constants, as a type that selects the paper's "Native" comparison
+// arithmetic (fig:native_shoup): every twiddle product is reduced
+// with the native 128-by-64-bit modulo, (unsigned __int128)(b w) % p, instead
+// of Shoup's modmul.  Only ntt_forward_variant(NTT_VARIANT_NATIVE) uses it.
+struct PrimeConstN : PrimeConst {
 };
 
 template <class C>
@@ -173,6 +180,12 @@ __device__ __forceinline__ uint64_t shoup(uint64_t b, const Tw& t, const PrimeCo
 {
     return shoup_lazy_p(b, t.w, t.wb, c.m1);
 }
+// Native modulo (PrimeConstN): exact, so the result is in [0, p) -- inside the
+// [0, 4p) range every butterfly bound assumes.
+__device__ __forceinline__ uint64_t shoup(uint64_t b, const Tw& t, const PrimeConstN& c)
+{
+    return (uint64_t)(((unsigned __int128)b * t.w) % c.p);
+}
 
 __device__ __forceinline__ uint64_t csub(uint64_t x, uint64_t m) { return x >= m ? x - m : x; }
 
@@ -267,6 +280,17 @@ __device__ __forceinline__ void gs_bf(uint64_t& X, uint64_t& Y, const W& w, cons
     X = x + y - (ge ? c.p4 : 0);
     Y = w.mul(x - y + c.p5, c);
 }
+
+// Programmatic dependent launch (PDL).  The kernels of a transform are
+// launched with programmatic stream serialization (ntt::launch_pdl), so the
+// next kernel's CTAs can be scheduled -- and stage their constant twiddles --
+// while this kernel's last wave still runs.  Every kernel lets its dependents
+// launch once all of its CTAs have started (pdl_trigger, at entry: no CTA of a
+// dependent can then hold a slot a CTA of this grid still needs) and waits for
+// its predecessor's completion and memory flush (pdl_wait) before its first
+// read or write of the data.  Both are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ Tw ldg_tw(const Tw* ptr)
 {

@@ -5,10 +5,12 @@
 
 namespace ntt {
 
-cudaError_t launch_fused(bool inverse, const KArgs& a, uint32_t rows, cudaStream_t st, bool proth)
+cudaError_t launch_fused(bool inverse, const KArgs& a, uint32_t rows, cudaStream_t st, int arith)
 {
-    return proth ? launch_fused_all<PrimeConstP>(inverse, a, rows, st)
-                 : launch_fused_all<PrimeConst>(inverse, a, rows, st);
+    switch (arith) {
+        case kArithProth: return launch_fused_all<PrimeConstP>(inverse, a, rows, st);
+        default: return launch_fused_all<PrimeConst>(inverse, a, rows, st);
+    }
 }
 
 }  // namespace ntt

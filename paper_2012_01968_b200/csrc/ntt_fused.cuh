@@ -26,6 +26,7 @@
 // cluster size).
 #pragma once
 #include "ntt_device.cuh"
+#include "ntt_launch.h"
 
 namespace ntt {
 
@@ -78,6 +79,8 @@ __global__ void __launch_bounds__(FusedCfg::CT, 2) k_fused(const KArgs a)
     constexpr int NR = SC::NR;
     constexpr int NOOT = 1 << 20;
     extern __shared__ __align__(16) uint64_t sm[];
+    pdl_trigger();
+    pdl_wait();
 
     const uint32_t tid = threadIdx.x;
     const uint32_t k = cluster_rank();       // block of the row this CTA owns
@@ -218,25 +221,20 @@ template <int LOGC, bool INV, class PCT>
 cudaError_t launch_fused_t(const KArgs& a, uint32_t rows, cudaStream_t st)
 {
     auto fn = k_fused<LOGC, INV, PCT>;
-    static std::atomic<uint64_t> attr_set{0};  // one bit per device
-    if (!detail::set_once(attr_set)) {
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FusedCfg::SMEM);
-        if ((1 << LOGC) > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(rows << LOGC);
-    cfg.blockDim = dim3(FusedCfg::CT);
-    cfg.dynamicSmemBytes = FusedCfg::SMEM;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 1u << LOGC;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, fn, a);
-    return cudaPeekAtLastError();
+    static DeviceOnce once;
+    if (cudaError_t e = once.run([&](int&) {
+            cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FusedCfg::SMEM);
+            if (r == cudaSuccess && (1 << LOGC) > 8)
+                r = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            return r;
+        }))
+        return e;
+    cudaLaunchAttribute cl;
+    cl.id = cudaLaunchAttributeClusterDimension;
+    cl.val.clusterDim.x = 1u << LOGC;
+    cl.val.clusterDim.y = 1;
+    cl.val.clusterDim.z = 1;
+    return launch_pdl(fn, dim3(rows << LOGC), dim3(FusedCfg::CT), FusedCfg::SMEM, st, a, &cl);
 }
 
 template <class PCT>

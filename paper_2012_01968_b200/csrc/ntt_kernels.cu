@@ -26,24 +26,31 @@ cudaError_t launch_pointwise(const KArgs& a, cudaStream_t st)
     const uint64_t words = ((uint64_t)a.batch * a.L) << a.logn;
     const uint64_t threads = (words + 1) / 2;
     k_pointwise<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(a, words);
-    return cudaPeekAtLastError();
+    return launch_status();
 }
 
-cudaError_t launch_single(bool inverse, const KArgs& a, int ots, uint32_t iters, cudaStream_t st, bool proth)
+cudaError_t launch_single(bool inverse, const KArgs& a, int ots, uint32_t iters, cudaStream_t st, int arith)
 {
-    return proth ? launch_single_p(inverse, a, ots, iters, st)
-                 : launch_single_t<PrimeConst>(inverse, a, ots, iters, st);
+    switch (arith) {
+        case kArithProth: return launch_single_p(inverse, a, ots, iters, st);
+        default: return launch_single_t<PrimeConst>(inverse, a, ots, iters, st);
+    }
 }
 
-cudaError_t launch_k2(bool inverse, int loge, const KArgs& a, int ots, uint32_t iters, cudaStream_t st, bool proth)
+cudaError_t launch_k2(bool inverse, int loge, const KArgs& a, int ots, uint32_t iters, cudaStream_t st, int arith)
 {
-    return proth ? launch_k2_p(inverse, loge, a, ots, iters, st)
-                 : launch_k2_t<PrimeConst>(inverse, loge, a, ots, iters, st);
+    switch (arith) {
+        case kArithProth: return launch_k2_p(inverse, loge, a, ots, iters, st);
+        default: return launch_k2_t<PrimeConst>(inverse, loge, a, ots, iters, st);
+    }
 }
 
-cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st, bool proth)
+cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st, int arith)
 {
-    return proth ? launch_k1_p(inverse, loge, a, rows, st) : launch_k1_t<PrimeConst>(inverse, loge, a, rows, st);
+    switch (arith) {
+        case kArithProth: return launch_k1_p(inverse, loge, a, rows, st);
+        default: return launch_k1_t<PrimeConst>(inverse, loge, a, rows, st);
+    }
 }
 
 }  // namespace ntt

@@ -55,6 +55,8 @@ __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>
     constexpr int M = SC::M, NR = SC::NR, CT = ColsCfg<LOGN1, LOGE>::CT;
     extern __shared__ __align__(16) uint64_t sm[];  // [M][16] words, then Tw[M]
     Tw* tws = reinterpret_cast<Tw*>(sm + M * 16);
+    pdl_trigger();
+    pdl_wait();
 
     const uint32_t tid = threadIdx.x, c = tid & 15u, tib = tid >> 4;
     const uint32_t tile = blockIdx.x & ((1u << a.log_tiles) - 1u);
@@ -178,6 +180,8 @@ __global__ void __launch_bounds__(ColsPipeCfg<LOGN1, LOGE>::CT, ColsPipeCfg<LOGN
     constexpr int M = SC::M, NR = SC::NR, CT = CC::CT;
     constexpr uint32_t logn2 = LOGN - LOGN1;
     extern __shared__ __align__(16) uint64_t sm[];
+    pdl_trigger();
+    pdl_wait();
     auto tile_of = [&](uint32_t buf) { return sm + buf * (CC::BUF / 8); };
     auto tw_of = [&](uint32_t buf) { return reinterpret_cast<Tw*>(sm + buf * (CC::BUF / 8) + M * 16); };
 
@@ -325,6 +329,8 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
     constexpr int M = SC::M, E = SC::E, TB = SC::TB, NR = SC::NR;
     constexpr int OT_FROM = OTS ? LOGM - OTS : (1 << 20);
     extern __shared__ __align__(16) uint64_t sm[];
+    pdl_trigger();
+    pdl_wait();
 
     const uint32_t tid = threadIdx.x, blk = tid / TB, tib = tid % TB;
     uint64_t* sb = sm + blk * M;
@@ -519,6 +525,7 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
     constexpr int OT_FROM = OTS ? LOGM - OTS : (1 << 20);
     extern __shared__ __align__(16) uint64_t sm[];
     Tw* const tws = reinterpret_cast<Tw*>(sm + NB * M);
+    pdl_trigger();
 
     const uint32_t tid = threadIdx.x, blk = tid / TB, tib = tid % TB;
     // CTA -> (l, bb, ciphertext group), prime-major then block position
@@ -539,6 +546,7 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
         for (uint32_t i = tid; i < USED; i += CT) cp_async16(tws + i, t2 + i);
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
+    pdl_wait();  // the twiddles are constant: staged while the previous kernel finishes
     uint64_t* sb = sm + blk * M;
     auto tabf = [&](const TwKey& k) {
         return tws[K2Layout<LOGM, LE2>::round_off(k.S) + ((((1u << k.i) - 1u + k.h) << k.S) + k.g)];
@@ -780,9 +788,11 @@ __global__ void __launch_bounds__(PipeCfg<LOGM, LOGE>::CT, PipeCfg<LOGM, LOGE>::
     };
     auto commit = [] { asm volatile("cp.async.commit_group;" ::: "memory"); };
 
+    pdl_trigger();
     uint32_t gb = blockIdx.x * NB + blk;
+    prefetch_tw(gb);  // constant: staged while the previous kernel finishes
+    pdl_wait();
     prefetch_data(gb, 0);
-    prefetch_tw(gb);
     commit();
     for (uint32_t it = 0; gb < a.total_blocks; ++it, gb += nslots) {
         uint64_t* sb = sm + ((it & 1) * NB + blk) * M;
@@ -917,25 +927,18 @@ inline int sm_count()
     return v;
 }
 
-// true if this device already had the attribute set; marks it otherwise
-inline bool set_once(std::atomic<uint64_t>& mask)
-{
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const uint64_t bit = 1ull << (dev & 63);
-    return mask.fetch_or(bit) & bit;
-}
-
 template <int LOGN1, int LOGN, int LOGE, bool INV, class PCT>
 cudaError_t launch_cols_t(const KArgs& a, uint32_t rows, cudaStream_t st)
 {
     using CC = ColsCfg<LOGN1, LOGE>;
     auto fn = k_cols<LOGN1, LOGN, LOGE, INV, PCT>;
-    static std::atomic<uint64_t> attr_set{0};  // one bit per device
-    if (!set_once(attr_set)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
+    static DeviceOnce once;
+    if (cudaError_t e = once.run([&](int&) {
+            return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
+        }))
+        return e;
     const uint64_t grid = (uint64_t)rows << a.log_tiles;
-    fn<<<(unsigned)grid, CC::CT, CC::SMEM, st>>>(a);
-    return cudaPeekAtLastError();
+    return launch_pdl(fn, dim3((unsigned)grid), dim3(CC::CT), CC::SMEM, st, a);
 }
 
 template <int LOGM, int LOGE, bool INV, bool FUSE0, int OTS, bool TWS, bool MUL, class PCT>
@@ -943,13 +946,15 @@ cudaError_t launch_contig_t(KArgs a, uint32_t iters, cudaStream_t st)
 {
     using CC = ContigCfg<LOGM, LOGE, TWS>;
     auto fn = k_contig<LOGM, LOGE, INV, FUSE0, OTS, TWS, MUL, PCT>;
-    static std::atomic<uint64_t> attr_set{0};  // one bit per device
-    if (!set_once(attr_set)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
+    static DeviceOnce once;
+    if (cudaError_t e = once.run([&](int&) {
+            return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
+        }))
+        return e;
     a.iters = iters;
     const uint64_t per_cta = (uint64_t)CC::NB * iters;
     const uint64_t grid = (a.total_blocks + per_cta - 1) / per_cta;
-    fn<<<(unsigned)grid, CC::CT, CC::SMEM, st>>>(a);
-    return cudaPeekAtLastError();
+    return launch_pdl(fn, dim3((unsigned)grid), dim3(CC::CT), CC::SMEM, st, a);
 }
 
 template <int LOGM, int LOGE, bool INV, int OTS, bool MUL, class PCT>
@@ -957,17 +962,17 @@ cudaError_t launch_blocks_t(KArgs a, cudaStream_t st)
 {
     using PC = PipeCfg<LOGM, LOGE>;
     auto fn = k_blocks<LOGM, LOGE, INV, OTS, MUL, PCT>;
-    static std::atomic<uint64_t> attr_set{0};  // one bit per device
-    static int ctas_per_sm = 0;
-    if (!set_once(attr_set)) {
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC::SMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, fn, PC::CT, PC::SMEM);
-    }
+    static DeviceOnce once;  // value: resident CTAs per SM
+    if (cudaError_t e = once.run([&](int& ctas) {
+            cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC::SMEM);
+            return r != cudaSuccess ? r : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, fn, PC::CT, PC::SMEM);
+        }))
+        return e;
+    const int ctas_per_sm = once.value();
     const int sms = sm_count();
     const uint64_t want = ((uint64_t)a.total_blocks + PC::NB - 1) / PC::NB;
     const uint64_t grid = std::min<uint64_t>(want, (uint64_t)sms * std::max(1, ctas_per_sm));
-    fn<<<(unsigned)grid, PC::CT, PC::SMEM, st>>>(a);
-    return cudaPeekAtLastError();
+    return launch_pdl(fn, dim3((unsigned)grid), dim3(PC::CT), PC::SMEM, st, a);
 }
 
 template <int LOGM, bool INV, int OTS, bool MUL, class PCT, int LE2>
@@ -975,11 +980,13 @@ cudaError_t launch_shared_t(const KArgs& a, cudaStream_t st)
 {
     using CC = SharedCfg<LOGM, INV>;
     auto fn = k_shared<LOGM, INV, OTS, MUL, PCT, LE2>;
-    static std::atomic<uint64_t> attr_set{0};  // one bit per device
-    if (!set_once(attr_set)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
+    static DeviceOnce once;
+    if (cudaError_t e = once.run([&](int&) {
+            return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
+        }))
+        return e;
     const uint64_t grid = ((uint64_t)a.L << a.log_n1) * ((a.batch + CC::NB - 1) / CC::NB);
-    fn<<<(unsigned)grid, CC::CT, CC::SMEM, st>>>(a);
-    return cudaPeekAtLastError();
+    return launch_pdl(fn, dim3((unsigned)grid), dim3(CC::CT), CC::SMEM, st, a);
 }
 
 template <int LOGM, bool INV, class PCT, int LE2>
@@ -1078,17 +1085,17 @@ cudaError_t launch_cols_pipe_t(const KArgs& a, uint32_t rows, cudaStream_t st)
 {
     using CC = ColsPipeCfg<LOGN1, LOGE>;
     auto fn = k_cols_pipe<LOGN1, LOGN, LOGE, INV, PCT>;
-    static std::atomic<uint64_t> attr_set{0};  // one bit per device
-    static int ctas_per_sm = 0;
-    if (!set_once(attr_set)) {
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, fn, CC::CT, CC::SMEM);
-    }
+    static DeviceOnce once;  // value: resident CTAs per SM
+    if (cudaError_t e = once.run([&](int& ctas) {
+            cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
+            return r != cudaSuccess ? r : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, fn, CC::CT, CC::SMEM);
+        }))
+        return e;
+    const int ctas_per_sm = once.value();
     const int sms = sm_count();
     const uint64_t want = (uint64_t)rows << a.log_tiles;
     const uint64_t grid = std::min<uint64_t>(want, (uint64_t)sms * std::max(1, ctas_per_sm));
-    fn<<<(unsigned)grid, CC::CT, CC::SMEM, st>>>(a);
-    return cudaPeekAtLastError();
+    return launch_pdl(fn, dim3((unsigned)grid), dim3(CC::CT), CC::SMEM, st, a);
 }
 
 template <bool INV, class PCT, int... Ks>

@@ -1,21 +1,86 @@
 // ntt_launch.h -- host-side launchers of the kernels in ntt_kernels.cuh.
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 #include "ntt_device.cuh"
 
 namespace ntt {
-// proth: every prime of the plan is = 1 mod 2^32 -> the PrimeConstP arithmetic
-// (default kernel variants only; see ntt_kernels.cuh).
+// One-time, per-device setup of a kernel (cudaFuncSetAttribute, occupancy
+// query), safe from any number of host threads: the first caller on a device
+// runs `f` under the mutex and the device's bit is published only after `f`
+// succeeded, so no thread launches before the attribute is in place; a failed
+// setup is retried by the next call.  value(dev) holds what `f` stored.
+struct DeviceOnce {
+    std::atomic<uint64_t> done{0};
+    std::mutex mu;
+    int val[64] = {};
+    template <class F>
+    cudaError_t run(F&& f)
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return cudaGetLastError();
+        const uint64_t bit = 1ull << (dev & 63);
+        if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+        std::lock_guard<std::mutex> lk(mu);
+        if (done.load(std::memory_order_relaxed) & bit) return cudaSuccess;
+        const cudaError_t e = f(val[dev & 63]);
+        if (e != cudaSuccess) {
+            cudaGetLastError();  // consume it: reported once, here
+            return e;
+        }
+        done.fetch_or(bit, std::memory_order_release);
+        return cudaSuccess;
+    }
+    int value()
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        return val[dev & 63];
+    }
+};
+// Error of the launch just made: cudaGetLastError consumes it, so one failed
+// launch is reported once and does not poison later calls on the thread.
+inline cudaError_t launch_status() { return cudaGetLastError(); }
+
+// Launch a transform kernel with programmatic stream serialization (PDL, see
+// pdl_trigger / pdl_wait in ntt_device.cuh); the status of the launch.
+template <class K>
+cudaError_t launch_pdl(void (*fn)(K), dim3 grid, dim3 block, size_t smem, cudaStream_t st, const K& a,
+                       const cudaLaunchAttribute* extra = nullptr)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    unsigned n = 1;
+    if (extra) at[n++] = *extra;
+    cfg.attrs = at;
+    cfg.numAttrs = n;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fn, a);
+    return e != cudaSuccess ? (cudaGetLastError(), e) : launch_status();
+}
+
+// arith: the prime-constant type the kernels are instantiated on --
+// kArithGeneral (PrimeConst, any prime) or kArithProth (PrimeConstP: every
+// prime = 1 mod 2^32); DESIGN.md 5.1.  The Proth form exists for the default
+// kernel variants only (ntt_kernels.cuh).
+enum { kArithGeneral = 0, kArithProth = 1 };
 // One kernel per row: contiguous rows of N = 2^logn, N <= 2^13.
 cudaError_t launch_single(bool inverse, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st,
-                          bool proth = false);
+                          int arith = kArithGeneral);
 // Kernel-2 (forward) / Kernel-2' (inverse): contiguous N2-blocks.
-// loge: per-thread radix 2^loge (3 or 4).
+// loge: the Kernel-2 variant (9 = default).
 cudaError_t launch_k2(bool inverse, int loge, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st,
-                      bool proth = false);
+                      int arith = kArithGeneral);
 // Kernel-1 (forward) / Kernel-1' (inverse): stride-N2 columns, 16 per CTA.
-cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st, bool proth = false);
+cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st,
+                      int arith = kArithGeneral);
 // the Proth instantiations (ntt_kernels_p.cu)
 cudaError_t launch_single_p(bool inverse, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
 cudaError_t launch_k2_p(bool inverse, int loge, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
@@ -23,11 +88,14 @@ cudaError_t launch_k1_p(bool inverse, int loge, const KArgs& a, uint32_t rows, c
 // Single-pass NTT / iNTT, one thread-block cluster per row (N = 2^14..2^17;
 // ntt_fused.cuh).  a.tab2 must be the Kernel-2-ordered table of the split
 // N = (N / 2^13) x 2^13.
-cudaError_t launch_fused(bool inverse, const KArgs& a, uint32_t rows, cudaStream_t st, bool proth);
+cudaError_t launch_fused(bool inverse, const KArgs& a, uint32_t rows, cudaStream_t st, int arith);
 // data <- mul_a (.) data 2^-64 (Montgomery), every word.
 cudaError_t launch_pointwise(const KArgs& a, cudaStream_t st);
 // The paper's comparison kernels, forward only: 1 = radix-2 per stage, 2 = register radix-16.
 cudaError_t launch_baseline_forward(int variant, const KArgs& a, cudaStream_t st);
+// The paper's "Native" arm: the default forward kernels with native-modulo twiddle products
+// (ntt_native.cu); cudaErrorNotSupported for a non-default split.
+cudaError_t launch_native_forward(KArgs a, uint32_t rows, cudaStream_t st);
 // 32-bit-word path: all passes of one direction.
 cudaError_t launch32(bool inverse, const KArgs32& a, uint32_t rows, cudaStream_t st);
 }  // namespace ntt

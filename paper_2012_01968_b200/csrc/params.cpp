@@ -89,7 +89,10 @@ Twiddle32 shoup_pair32(uint32_t w, uint32_t p)
 
 bool valid_ntt_prime(uint64_t p, uint64_t N)
 {
-    return p < (1ull << 60) && p > 2 && (p - 1) % (2 * N) == 0 && is_prime_u64(p);
+    // [2^59, 2^60): the range P:423 names, and what the 64-bit kernels need --
+    // reduce_full's quotient estimate floor(2^90 / p) must fit 32 bits (p > 2^58)
+    // and the lazy bounds of DESIGN.md 5.1 need p < 2^60
+    return p >= (1ull << 59) && p < (1ull << 60) && (p - 1) % (2 * N) == 0 && is_prime_u64(p);
 }
 
 uint64_t smallest_psi(uint64_t p, uint64_t N)

@@ -66,7 +66,7 @@ void k2_order(const T* std_tab, unsigned logn, unsigned log_n1, unsigned loge, T
 // Smallest primitive 2N-th root of unity mod p (R2); 0 if none.
 uint64_t smallest_psi(uint64_t p, uint64_t N);
 
-// Validation used by plan creation: prime, p = 1 mod 2N, p < 2^60.
+// Validation used by plan creation: prime, p = 1 mod 2N, 2^59 <= p < 2^60.
 bool valid_ntt_prime(uint64_t p, uint64_t N);
 
 // Fills tab[i] = shoup_pair(root^bitrev_logn(i)) for i < N.

@@ -176,3 +176,65 @@ def test_proth_primes_errors():
     assert lib.ntt_find_primes_ex(1 << 12, 2, 7, out) == -3  # unknown form
     assert lib.ntt_find_primes_ex(3, 2, 1, out) == -1
     assert lib.ntt_find_primes_ex(1 << 12, 0, 1, out) == -3
+
+
+# ------------------------------------------------------------------ round 2: ADVICE / golden / Python-side checks
+
+def test_small_ntt_primes_rejected():
+    """Primes below 2^59 are rejected with INVALID_PRIME before the device is
+    touched (the 64-bit kernels need p > 2^58 for reduce_full's estimate and
+    P:423 names [2^59, 2^60)); (N=4, p=17) is a valid NTT prime otherwise."""
+    lib = _native.lib()
+    h = ctypes.c_void_p()
+    for n, p in [(4, 17), (256, 12289), (1 << 12, oracle.find_primes(1 << 12, 1, 1 << 58, 1 << 59)[0])]:
+        arr = (ctypes.c_uint64 * 1)(p)
+        assert lib.ntt_plan_create(ctypes.byref(h), n, arr, 1) == -2, (n, p)
+    p59 = oracle.find_primes(1 << 12, 1, 1 << 59, (1 << 59) + (1 << 40))  # the lowest accepted range
+    assert p59 and p59[0] >= 1 << 59
+
+
+def test_golden_shoup_companion(golden):
+    """w_bar(1,17) = floor(2^64/17), w_bar(0,17) = 0 -- the host
+    routine the plan tables are built with."""
+    from paper_2012_01968_b200 import shoup_companion
+    for g in golden["shoup"]:
+        assert shoup_companion(g["w"], g["p"]) == g["w_bar"], g["cite"]
+    with pytest.raises(NttError):
+        shoup_companion(17, 17)  # w >= p
+
+
+def test_golden_table_sizes(golden):
+    """P:92 / S:206-207 table bytes and P:795 OT entry count, from the function
+    plan creation sizes its allocations with."""
+    from paper_2012_01968_b200 import table_sizes
+    for g in golden["table_bytes"]:
+        t = table_sizes(g["N"], g["np"])
+        assert t["psi_bytes"] * g["directions"] == g["bytes"], g["cite"]
+    for g in golden["ot_entries"]:
+        assert table_sizes(g["N"], 1, g["base"])["ot_entries"] == g["entries"], g["cite"]
+    # a default C4 plan: Psi + Psi^-1, their Kernel-2 copies, OT bases, two 112-byte PrimeConst per prime
+    t = table_sizes(1 << 17, 60)
+    assert t["plan_bytes"] == 4 * 60 * (1 << 17) * 16 + 2 * 60 * 1152 * 16 + 2 * 60 * 112
+
+
+def test_execute_host_validates_host_buffers():
+    """Host buffers must be C-contiguous 64-bit integer CPU arrays:
+    a float / int32 array or a strided view is refused before the C ABI."""
+    import numpy as np
+    from paper_2012_01968_b200 import Plan
+    plan = Plan.__new__(Plan)  # no device here: only the argument checks run
+    plan.N, plan.L, plan._h = 8, 1, None
+    good = np.zeros(8, dtype=np.uint64)
+    for bad, err in [(np.zeros(8, dtype=np.int32), TypeError), (np.zeros(8, dtype=np.float64), TypeError),
+                     (np.zeros(16, dtype=np.uint64)[::2], ValueError), ([0] * 8, TypeError)]:
+        with pytest.raises(err):
+            plan.execute_host(bad, good, 3, None)
+        with pytest.raises(err):
+            plan.execute_host(good, bad, 3, None)
+
+
+def test_library_reads_no_environment():
+    """Kernel selection is an ntt_opts_t field, not an environment variable."""
+    srcs = glob.glob(os.path.join(ROOT, "paper_2012_01968_b200", "csrc", "*"))
+    for f in srcs:
+        assert "getenv" not in open(f).read(), f

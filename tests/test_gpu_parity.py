@@ -20,6 +20,12 @@ def _need_gpu():
 from paper_2012_01968_b200 import Plan, NttError, NTT_DIR_FORWARD, NTT_DIR_INVERSE  # noqa: E402
 
 
+def variant_kw(variant: str) -> dict:
+    """"k1,k2" -> the ntt_opts_t kernel-variant fields (k1 4 = the default)."""
+    k1, k2 = (int(v) for v in variant.split(","))
+    return {"k1_variant": k1, "k2_variant": k2}
+
+
 def to_dev(x: np.ndarray):
     return torch.from_numpy(np.ascontiguousarray(x).view(np.int64)).cuda()
 
@@ -247,15 +253,15 @@ def test_negacyclic_mul(logn, kw):
 
 
 @pytest.mark.parametrize("variant", ["4,3", "4,6", "4,4", "4,5"])
-def test_negacyclic_mul_unfused_variants(variant, monkeypatch):
+def test_negacyclic_mul_unfused_variants(variant):
     """Kernel-2 variants without the fused product fall back to a separate
     element-wise kernel: same result."""
-    monkeypatch.setenv("NTT_LOGE", variant)
+    kv = variant_kw(variant)
     N = 1 << 15
     primes, psis = chain(N, 2)
     a = synth.rns_rows(primes, 1, N, config_id=12)
     b = synth.rns_rows(primes, 1, N, config_id=13)
-    plan = Plan(N, primes)
+    plan = Plan(N, primes, **kv)
     da, db = to_dev(a), to_dev(b)
     plan.negacyclic_mul(da, db)
     A = oracle.ntt_batch(a.copy(), primes, psis, +1)
@@ -289,12 +295,12 @@ def test_c5_prime_sweep(L):
 
 @pytest.mark.parametrize("variant", ["4,3", "4,4", "4,5", "4,6", "4,7", "4,9", "5,5"])
 @pytest.mark.parametrize("logn,log_n1", [(14, 7), (15, 7), (16, 8), (17, 8), (17, 7), (17, 9)])
-def test_kernel2_variants(variant, logn, log_n1, monkeypatch):
+def test_kernel2_variants(variant, logn, log_n1):
     """Kernel-2 implementations (radix 8 / 16, one-shot / pipelined persistent)
-    selected with the NTT_LOGE tuning knob: all bit-exact, OT on and off."""
-    monkeypatch.setenv("NTT_LOGE", variant)
-    check_roundtrip(1 << logn, 3, 2, log_n1=log_n1)
-    check_roundtrip(1 << logn, 2, 1, log_n1=log_n1, ot=True)
+    selected with ntt_opts_t.k1_variant / k2_variant: all bit-exact, OT on and off."""
+    kv = variant_kw(variant)
+    check_roundtrip(1 << logn, 3, 2, log_n1=log_n1, **kv)
+    check_roundtrip(1 << logn, 2, 1, log_n1=log_n1, ot=True, **kv)
 
 
 @pytest.mark.parametrize("logn", [14, 15, 16, 17])

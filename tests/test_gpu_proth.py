@@ -21,6 +21,12 @@ def _need_gpu():
 from paper_2012_01968_b200 import Plan  # noqa: E402
 
 
+def variant_kw(variant: str) -> dict:
+    """"k1,k2" -> the ntt_opts_t kernel-variant fields (k1 4 = the default)."""
+    k1, k2 = (int(v) for v in variant.split(","))
+    return {"k1_variant": k1, "k2_variant": k2}
+
+
 def to_dev(x: np.ndarray):
     return torch.from_numpy(np.ascontiguousarray(x).view(np.int64)).cuda()
 
@@ -141,8 +147,8 @@ def test_proth_full_size_c4():
 
 @pytest.mark.parametrize("variant", ["4,5", "4,7", "4,9", "5,7"])
 @pytest.mark.parametrize("logn,log_n1", [(14, 7), (16, 8), (17, 8), (17, 6), (17, 9)])
-def test_proth_kernel_variants(variant, logn, log_n1, monkeypatch):
-    """Kernel variants with Proth instantiations (NTT_LOGE knob), OT on and off."""
-    monkeypatch.setenv("NTT_LOGE", variant)
-    roundtrip(1 << logn, 3, 2, log_n1=log_n1)
-    roundtrip(1 << logn, 2, 3, log_n1=log_n1, ot=True)
+def test_proth_kernel_variants(variant, logn, log_n1):
+    """Kernel variants with Proth instantiations (k1_variant / k2_variant), OT on and off."""
+    kv = variant_kw(variant)
+    roundtrip(1 << logn, 3, 2, log_n1=log_n1, **kv)
+    roundtrip(1 << logn, 2, 3, log_n1=log_n1, ot=True, **kv)

@@ -3,6 +3,7 @@
 // practical ALU ceiling the NTT kernels are measured against.  Each thread
 // runs radix-16 rounds (4 stages x 8 butterflies) on 16 registers, no memory.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -o tools/libs/bf_roof tools/bf_roof.cu
+// (__graft_entry__.build() does this; bench.py runs it for the live ceiling of its roofline line).
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -34,9 +35,11 @@ __global__ void __launch_bounds__(256, 4) k_bf(uint64_t* out, const Tw* tw, cons
                     else ct_bf(x[k], x[k + half], w, c, red);
                 }
         }
-        if constexpr (GS) {  // keep the GS values bounded like the kernels' rounds do
+        if constexpr (GS) {  // bound the GS values (< 4p + 2^(32+s) after s stages) every 16 stages,
+            if ((it & 3) == 3) {  // less often than the kernels' own final normalisation costs
 #pragma unroll
-            for (int i = 0; i < 16; ++i) x[i] = norm4(csub(x[i], c.p4), c);
+                for (int i = 0; i < 16; ++i) x[i] = norm4(csub(x[i], c.p4), c);
+            }
         }
     }
     uint64_t s = 0;
