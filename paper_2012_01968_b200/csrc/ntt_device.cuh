@@ -244,6 +244,12 @@ struct TwMul<true> {
 //     output and input stay below 12p + 2^32:
 //     red = 2: X <- X mod* 8p (< 8p + 2^32), outputs < 12p + 2^32;
 //     red = 0: no reduction, inputs < 12p + 2^32, outputs < 16p + 2^32.
+//   red = 3 / 0 (any other prime, p < 2^60, so 16p < 2^64): the same every-
+//     other-stage pattern with an exact 64-bit compare (two ISETPs instead of
+//     one), so no 2^32 excess accumulates:
+//     red = 3: X <- X mod 8p (< 8p), outputs < 12p;
+//     red = 0: inputs < 12p (< 13p after a canonical input's first stages),
+//     outputs < 16p.
 // The conditional subtraction is decided on the high words (csub_hi) and
 // folded into both outputs as 3-input adds (IADD3 / IADD3.X on the ALU pipe;
 // a 2-input 64-bit add lets ptxas emit IMAD.X on the multiply pipe).
@@ -257,9 +263,11 @@ __device__ __forceinline__ void ct_bf(uint64_t& X, uint64_t& Y, const W& w, cons
         Y = x - t + c.p4;
         return;
     }
-    const bool ge = red == 2 ? (uint32_t)(x >> 32) > c.p8_hi : (uint32_t)(x >> 32) > c.p4_hi;
-    const uint64_t s = ge ? (red == 2 ? c.p8 : c.p4) : 0;
-    const uint64_t s2 = red == 2 ? (ge ? 0 - c.p4 : c.p4) : (ge ? 0 : c.p4);
+    const bool ge = red == 3   ? x >= c.p8
+                    : red == 2 ? (uint32_t)(x >> 32) > c.p8_hi
+                               : (uint32_t)(x >> 32) > c.p4_hi;
+    const uint64_t s = ge ? (red >= 2 ? c.p8 : c.p4) : 0;
+    const uint64_t s2 = red >= 2 ? (ge ? 0 - c.p4 : c.p4) : (ge ? 0 : c.p4);
     const uint64_t t = w.mul(Y, c);
     X = x - s + t;
     Y = x - t + s2;
@@ -430,10 +438,11 @@ __device__ __forceinline__ void ct_roundN(uint64_t (&x)[NI][16], uint32_t tib, u
 #pragma unroll
         for (int i = 0; i < Geo::r; ++i) {
             const int half = R >> (i + 1);
-            // Proth primes: reduce on the kernel's last stage and every second one before it
-            const int red = std::is_same_v<C, PrimeConstP>
-                                ? ((((LOGM - 1 - (S + i) - (FINAL ? 1 : 0)) & 1) || (CANON && S + i < 2)) ? 0 : 2)
-                                : 1;
+            // reduce on the kernel's last stage and every second one before it
+            // (ct_bf: red 2 for Proth primes, 3 for any other)
+            const int red = ((((LOGM - 1 - (S + i) - (FINAL ? 1 : 0)) & 1) || (CANON && S + i < 2))
+                                 ? 0
+                                 : (std::is_same_v<C, PrimeConstP> ? 2 : 3));
 #pragma unroll
             for (int h = 0; h < (1 << i); ++h) {
                 const uint32_t idx = (B << i) + h;

@@ -1,5 +1,6 @@
-// ntt_kernels.cu -- general-prime instantiation of the kernels in
-// ntt_kernels.cuh, the public launchers (which route Proth-prime plans to
+// ntt_kernels.cu -- the general-prime Kernel-2 family of ntt_kernels.cuh, the
+// public launchers (which route to the per-family translation units: Kernel-1
+// in ntt_k1.cu, the single-CTA kernel in ntt_single.cu, Proth Kernel-2 in
 // ntt_kernels_p.cu) and the element-wise product kernel.
 #include "ntt_kernels.cuh"
 
@@ -33,7 +34,7 @@ cudaError_t launch_single(bool inverse, const KArgs& a, int ots, uint32_t iters,
 {
     switch (arith) {
         case kArithProth: return launch_single_p(inverse, a, ots, iters, st);
-        default: return launch_single_t<PrimeConst>(inverse, a, ots, iters, st);
+        default: return launch_single_g(inverse, a, ots, iters, st);
     }
 }
 
@@ -49,7 +50,7 @@ cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cud
 {
     switch (arith) {
         case kArithProth: return launch_k1_p(inverse, loge, a, rows, st);
-        default: return launch_k1_t<PrimeConst>(inverse, loge, a, rows, st);
+        default: return launch_k1_g(inverse, loge, a, rows, st);
     }
 }
 

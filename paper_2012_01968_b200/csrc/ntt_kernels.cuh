@@ -29,6 +29,11 @@
 #include <atomic>
 #include <type_traits>
 
+// CTAs per SM the forward shared-twiddle Kernel-2 is compiled for (tuning constant)
+#ifndef NTT_K2_FWD_MINB
+#define NTT_K2_FWD_MINB 3
+#endif
+
 namespace ntt {
 
 // 16-byte asynchronous global -> shared copy (LDGSTS), and its completion.
@@ -513,7 +518,7 @@ struct SharedCfg {
     static constexpr size_t SMEM = (size_t)NB * (8u << LOGM) + (sizeof(Tw) << LOGM);
     // measured on C4: the forward (final reduction, more live values) runs
     // faster with 85 registers at 3 CTAs/SM, the inverse with 64 at 4
-    static constexpr int MINB = INV ? 4 : 3;
+    static constexpr int MINB = INV ? 4 : NTT_K2_FWD_MINB;
 };
 
 template <int LOGM, bool INV, int OTS, bool MUL = false, class PCT = PrimeConst, int LE2 = 4>

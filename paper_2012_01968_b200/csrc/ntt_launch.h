@@ -81,9 +81,12 @@ cudaError_t launch_k2(bool inverse, int loge, const KArgs& a, int ot_stages, uin
 // Kernel-1 (forward) / Kernel-1' (inverse): stride-N2 columns, 16 per CTA.
 cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st,
                       int arith = kArithGeneral);
-// the Proth instantiations (ntt_kernels_p.cu)
+// per-family instantiations, one translation unit each (parallel compilation):
+// _g general primes, _p Proth primes (ntt_single.cu, ntt_kernels_p.cu, ntt_k1.cu)
+cudaError_t launch_single_g(bool inverse, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
 cudaError_t launch_single_p(bool inverse, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
 cudaError_t launch_k2_p(bool inverse, int loge, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
+cudaError_t launch_k1_g(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st);
 cudaError_t launch_k1_p(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st);
 // Single-pass NTT / iNTT, one thread-block cluster per row (N = 2^14..2^17;
 // ntt_fused.cuh).  a.tab2 must be the Kernel-2-ordered table of the split

@@ -26,7 +26,8 @@ __global__ void __launch_bounds__(256, 4) k_bf(uint64_t* out, const Tw* tw, cons
         for (int st = 0; st < 4; ++st) {
             const int half = 8 >> st;
             const TwMul<false> w{stw[(st + it) & 3]};  // SMEM broadcast, as in the kernels
-            const int red = std::is_same_v<C, PrimeConstP> ? (((3 - st) & 1) ? 0 : 2) : 1;
+            // the kernels' pattern: reduce on every other stage (ct_bf red 2 Proth / 3 general)
+            const int red = ((3 - st) & 1) ? 0 : (std::is_same_v<C, PrimeConstP> ? 2 : 3);
 #pragma unroll
             for (int g = 0; g < 16; g += 2 * half)
 #pragma unroll

@@ -1,4 +1,4 @@
-"""Kernel-1 variants on C4 (experiment): NTT_LOGE k1 = 4 (one tile per CTA)
+"""Kernel-1 variants on C4 (experiment): k1_variant 4 (one tile per CTA)
 vs 5 (persistent, cp.async double buffer), per prime family; per-pass ms."""
 import json
 import os
@@ -22,8 +22,8 @@ for form in ["proth", "2n"]:
     d = torch.from_numpy(x.view(np.int64)).cuda()
     ref = d.clone()
     for var in variants:
-        os.environ["NTT_LOGE"] = var
-        plan = Plan(N, primes, fused=False)
+        k1, k2 = (int(v) for v in var.split(","))
+        plan = Plan(N, primes, fused=False, k1_variant=k1, k2_variant=k2)
         seq = [(NTT_DIR_FORWARD, 0), (NTT_DIR_FORWARD, 1), (NTT_DIR_INVERSE, 0), (NTT_DIR_INVERSE, 1)]
         for _ in range(3):
             plan.forward(d)

@@ -1,6 +1,7 @@
 """Summarise ncu reports for profiles/ (committed evidence).
 
     python tools/ncu_summary.py gpurun_out/prof.ncu-rep [more.ncu-rep] > profiles/rNN_ncu_summary.md
+    (every report argument may also be the CSV export of its raw page)
     python tools/ncu_summary.py --launches gpurun_out/launches.csv          (launch list -> shares)
     python tools/ncu_summary.py --traffic gpurun_out/prof.ncu-rep           (per-kernel DRAM bytes JSON)
 """
@@ -28,7 +29,12 @@ KEYS = [
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """The raw page of a report (.ncu-rep, read with ncu) or of its CSV export
+    (`ncu -i rep --page raw --csv > raw.csv`, e.g. made on the GPU box)."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     return rows[0], rows[1], rows[2:]
 

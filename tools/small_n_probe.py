@@ -9,8 +9,8 @@ for logn in (14, 15):
     x = synth.rns_rows(primes, 1, N, config_id=17)
     d = torch.from_numpy(x.view(np.int64)).cuda()
     for var in ["4,5", "4,7", "4,4", "4,3", "5,5"]:
-        os.environ["NTT_LOGE"] = var
-        plan = Plan(N, primes)
+        k1, k2 = (int(v) for v in var.split(","))
+        plan = Plan(N, primes, k1_variant=k1, k2_variant=k2)
         for _ in range(5):
             plan.forward(d)
         torch.cuda.synchronize()

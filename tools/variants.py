@@ -2,7 +2,7 @@
 
     python tools/variants.py [--config C4] [--steps 10] [--ot] [--log-n1 K]
 
-Variants are selected with the NTT_LOGE="k1,k2" knob read at plan creation.
+Variants "k1,k2" are the ntt_opts_t k1_variant / k2_variant fields.
 """
 import argparse
 import json
@@ -37,8 +37,8 @@ host = torch.from_numpy(x.view(np.int64))
 d = host.cuda()
 rows = B * L
 for var in a.variants.split(";"):
-    os.environ["NTT_LOGE"] = var
-    plan = Plan(N, primes, ot=a.ot, log_n1=a.log_n1)
+    k1, k2 = (int(v) for v in var.split(","))
+    plan = Plan(N, primes, ot=a.ot, log_n1=a.log_n1, k1_variant=k1, k2_variant=k2)
     info = plan.info()
     seq = [(NTT_DIR_FORWARD, i) for i in range(plan.passes)] + [(NTT_DIR_INVERSE, i) for i in range(plan.passes)]
     for _ in range(3):
