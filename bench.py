@@ -21,7 +21,8 @@ after timing, the per-row checksums that rank 0 checks against the oracle.
 --config C5 (mixed request stream, N=2^16, L swept over 1..45): throughput
 mode (whole requests round-robin to ranks, batched per L) and latency mode
 (one request at a time, its primes sharded over the ranks, replayed from a
-request graph), microseconds per request for each L.
+request graph -- the split's kernels or the one-kernel request, the faster
+per L), microseconds per request for each L.
 
 Prints ONE JSON line on rank 0 (DESIGN.md section 7 explains every key).
 """
@@ -717,11 +718,12 @@ def c5_line(D, args):
     per L, throughput mode (requests round-robin to ranks, each rank's
     requests of one L batched into one call) and latency mode (one request at
     a time, its primes sharded over the ranks, replayed from a request
-    graph).  value = mixed-stream latency-mode us per request (the mean over
+    graph: the split's kernels, or the one-kernel request of
+    NTT_GRAPH_ONE_KERNEL -- both timed, the faster one reported per L).  value = mixed-stream latency-mode us per request (the mean over
     the L sweep, one request per L in turn)."""
     torch = D.torch
     import synth
-    from paper_2012_01968_b200 import NTT_DIR_FORWARD, NTT_DIR_INVERSE, Plan, find_primes
+    from paper_2012_01968_b200 import NTT_DIR_FORWARD, NTT_DIR_INVERSE, NTT_GRAPH_ONE_KERNEL, Plan, find_primes
 
     rank, world = D.rank, D.world
     logn = 16
@@ -756,7 +758,7 @@ def c5_line(D, args):
         tp_plan.close()
         # latency: this rank's prime range of ONE request, replayed from a request graph
         off, n = prime_ranges(world, L)[rank] if world <= L else ((rank, 1) if rank < L else (0, 0))
-        lat_ms = 0.0
+        forms = {"graph": 0.0, "one_kernel": 0.0}
         if n > 0:
             lp = Plan(N, primes_all[off: off + n])
             y = torch.empty(n * N, dtype=torch.int64)
@@ -764,28 +766,36 @@ def c5_line(D, args):
                            out=y.numpy().view(np.uint64).reshape(1, n, N))
             yd = y.cuda()
             yref = yd.clone()
-            g = lp.graph(yd, NTT_DIR_FORWARD | NTT_DIR_INVERSE)
-            for _ in range(max(3, args.warmup)):
-                g.launch()
-            reps = max(20, args.steps * 4)
-            D.barrier()
-            torch.cuda.synchronize()
-            evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
-            evs[0].record()
-            for i in range(reps):  # one request in flight: each replay waits for the previous on the stream
-                g.launch()
-                evs[i + 1].record()
-            torch.cuda.synchronize()
-            lat_ms = statistics.median(evs[i].elapsed_time(evs[i + 1]) for i in range(reps))
-            launches += reps * 2 * lp.passes
-            ok_all = ok_all and bool(torch.equal(yd, yref))
-            g.close()
+            # two request forms: the split's kernels (2 per direction) captured
+            # as a graph, and the one-kernel request (NTT_GRAPH_ONE_KERNEL)
+            for form, flag, kernels in (("graph", 0, 2 * lp.passes), ("one_kernel", NTT_GRAPH_ONE_KERNEL, 1)):
+                g = lp.graph(yd, NTT_DIR_FORWARD | NTT_DIR_INVERSE | flag)
+                for _ in range(max(3, args.warmup)):
+                    g.launch()
+                reps = max(20, args.steps * 4)
+                D.barrier()
+                torch.cuda.synchronize()
+                evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+                evs[0].record()
+                for i in range(reps):  # one request in flight: each replay waits for the previous on the stream
+                    g.launch()
+                    evs[i + 1].record()
+                torch.cuda.synchronize()
+                forms[form] = statistics.median(evs[i].elapsed_time(evs[i + 1]) for i in range(reps))
+                launches += reps * kernels
+                ok_all = ok_all and bool(torch.equal(yd, yref))
+                g.close()
             lp.close()
         else:
             D.barrier()
-        lat_ms = max(D.allreduce([lat_ms], "max"))
+            D.barrier()
+        forms = {k: max(D.allreduce([v], "max")) for k, v in sorted(forms.items())}
+        lat_form = min(forms, key=forms.get)  # the faster request form at this L
+        lat_ms = forms[lat_form]
         sweep[str(L)] = {"throughput_us_per_request": round(tp_ms * 1e3 / C5_REQUESTS, 3),
                          "latency_us_per_request": round(lat_ms * 1e3, 3),
+                         "latency_form": lat_form,
+                         "latency_us_by_form": {k: round(v * 1e3, 3) for k, v in forms.items()},
                          "latency_primes_per_rank": [c for _, c in prime_ranges(world, L)] if world <= L
                          else [1 if r < L else 0 for r in range(world)]}
     ok_all = bool(D.allreduce([float(ok_all)], "min")[0])

@@ -264,10 +264,22 @@ ntt_status_t ntt_plan_destroy(ntt_plan_t plan);
  * DEVICE pointers as for ntt_forward; they are baked into the graph and must
  * stay valid while it exists.  The graph holds a reference to the plan's
  * tables: destroy the graph before the plan.  Synchronous; enqueues nothing.
+ *
+ * NTT_GRAPH_ONE_KERNEL (or'ed with the direction flags): the request is ONE
+ * cooperative kernel instead of two per direction -- the column and block
+ * passes of the split run as phases of one persistent grid with
+ * grid barriers between them (ntt_request.cu), for the
+ * latency of small requests (BASELINE config 5).  Results are identical to
+ * the two-kernel path's.  The graph then owns 8 bytes of device memory (the
+ * barrier state).  Requires N = 2^14..2^17, OT off, and a job the device can
+ * hold co-resident in one wave of its grid (any batch works; large jobs are
+ * faster without the flag).
  * Errors: as ntt_forward, INVALID_ARG (graph NULL, flags 0 or unknown,
- * batch 0, data2 NULL with NTT_GRAPH_PRODUCT), CUDA (capture failed). */
+ * batch 0, data2 NULL with NTT_GRAPH_PRODUCT, ONE_KERNEL with PRODUCT, OT,
+ * or N outside 2^14..2^17), CUDA (capture failed). */
 typedef struct ntt_graph_s *ntt_graph_t;
 #define NTT_GRAPH_PRODUCT 4u
+#define NTT_GRAPH_ONE_KERNEL 8u
 ntt_status_t ntt_graph_create(ntt_graph_t *graph, ntt_plan_t plan, uint64_t *data, uint64_t *data2, unsigned batch,
                               unsigned flags);
 

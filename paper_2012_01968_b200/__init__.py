@@ -14,11 +14,13 @@ from __future__ import annotations
 
 import ctypes
 
-from ._native import (NTT_ARITH_PROTH, NTT_DIR_FORWARD, NTT_DIR_INVERSE, NTT_GRAPH_PRODUCT, NTT_PRIMES_2N,
+from ._native import (NTT_ARITH_PROTH, NTT_DIR_FORWARD, NTT_DIR_INVERSE, NTT_GRAPH_ONE_KERNEL, NTT_GRAPH_PRODUCT,
+                      NTT_PRIMES_2N,
                       NTT_PRIMES_PROTH32, NttError, Opts, check, lib)
 
 __all__ = ["Plan", "Plan32", "Graph", "find_primes", "find_primes32", "find_psi", "table_sizes", "shoup_companion",
-           "NttError", "NTT_DIR_FORWARD", "NTT_DIR_INVERSE", "NTT_GRAPH_PRODUCT"]
+           "NttError", "NTT_DIR_FORWARD", "NTT_DIR_INVERSE", "NTT_GRAPH_PRODUCT",
+           "NTT_GRAPH_ONE_KERNEL"]
 
 
 PRIME_FORMS = {"2n": NTT_PRIMES_2N, "proth": NTT_PRIMES_PROTH32}
@@ -234,7 +236,8 @@ class Plan:
     def graph(self, x, flags: int = NTT_DIR_FORWARD | NTT_DIR_INVERSE, other=None) -> "Graph":
         """Capture the transforms `flags` of the CUDA tensor x (or, with
         NTT_GRAPH_PRODUCT, the product other <- x * other) into a replayable
-        request graph (ntt_graph_create)."""
+        request graph (ntt_graph_create).  | NTT_GRAPH_ONE_KERNEL: the whole
+        request as one cooperative kernel (N = 2^14..2^17, no OT)."""
         return Graph(self, x, flags, other)
 
     def corrupt_twiddle(self, direction: int, l: int, index: int, field: int, mask: int) -> None:

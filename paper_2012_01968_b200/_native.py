@@ -21,6 +21,7 @@ NTT_VARIANT_DEFAULT, NTT_VARIANT_RADIX2, NTT_VARIANT_RADIX16, NTT_VARIANT_NATIVE
 NTT_PRIMES_2N, NTT_PRIMES_PROTH32 = 0, 1
 NTT_ARITH_GENERAL, NTT_ARITH_PROTH = 0, 1
 NTT_GRAPH_PRODUCT = 4
+NTT_GRAPH_ONE_KERNEL = 8
 
 # every symbol include/ntt.h declares
 EXPORTS = [

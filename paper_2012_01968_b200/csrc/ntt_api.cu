@@ -661,7 +661,25 @@ struct ntt_graph_s {
     int device = 0;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    unsigned long long* bar = nullptr;  // NTT_GRAPH_ONE_KERNEL: grid barrier arrival counter
+    bool one = false;                  // NTT_GRAPH_ONE_KERNEL: ...
+    ntt::ReqArgs ra{};                 // its kernel arguments
+    unsigned logn = 0;
+    int arith = 0;
 };
+// NTT_REQ_DIRECT (experiment knob): replay a one-kernel request by launching
+// its kernel directly instead of through cudaGraphLaunch
+#ifndef NTT_REQ_DIRECT
+#define NTT_REQ_DIRECT 0
+#endif
+
+static void free_graph(ntt_graph_s* gr)
+{
+    if (gr->exec) cudaGraphExecDestroy(gr->exec);
+    if (gr->graph) cudaGraphDestroy(gr->graph);
+    if (gr->bar) cudaFree(gr->bar);
+    delete gr;
+}
 
 ntt_status_t ntt_graph_create(ntt_graph_t* out, ntt_plan_t plan, uint64_t* data, uint64_t* data2, unsigned batch,
                               unsigned flags)
@@ -669,9 +687,12 @@ ntt_status_t ntt_graph_create(ntt_graph_t* out, ntt_plan_t plan, uint64_t* data,
     NvtxRange r("ntt_graph_create");
     if (!out) return NTT_ERR_INVALID_ARG;
     *out = nullptr;
-    if (!plan || !data || batch == 0 || flags == 0 || (flags & ~7u)) return NTT_ERR_INVALID_ARG;
+    if (!plan || !data || batch == 0 || (flags & ~15u)) return NTT_ERR_INVALID_ARG;
     const bool product = flags & NTT_GRAPH_PRODUCT;
+    const bool one = flags & NTT_GRAPH_ONE_KERNEL;
+    if ((flags & 7u) == 0) return NTT_ERR_INVALID_ARG;
     if (product && (flags != NTT_GRAPH_PRODUCT || !data2 || data2 == data)) return NTT_ERR_INVALID_ARG;
+    if (one && (plan->logn < 14 || plan->logn > 17 || plan->ot_enable)) return NTT_ERR_INVALID_ARG;
     ntt_status_t s = check_data(plan, data);
     if (s == NTT_OK && product) s = check_data(plan, data2);
     if (s == NTT_OK) s = check_batch(plan, batch);
@@ -681,7 +702,17 @@ ntt_status_t ntt_graph_create(ntt_graph_t* out, ntt_plan_t plan, uint64_t* data,
     if (!gr) return NTT_ERR_OOM;
     gr->device = plan->device;
     cudaStream_t st = nullptr;
-    cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    cudaError_t e = cudaSuccess;
+    if (one) {
+        e = cudaMalloc(&gr->bar, ntt::kReqBarrierBytes);
+        if (e == cudaSuccess) e = cudaMemset(gr->bar, 0, ntt::kReqBarrierBytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            free_graph(gr);
+            return NTT_ERR_OOM;
+        }
+    }
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
         cudaError_t ek = cudaSuccess;
@@ -689,6 +720,21 @@ ntt_status_t ntt_graph_create(ntt_graph_t* out, ntt_plan_t plan, uint64_t* data,
             ek = enqueue(plan, data, batch, false, st);
             if (ek == cudaSuccess) ek = enqueue(plan, data2, batch, false, st);
             if (ek == cudaSuccess) ek = enqueue(plan, data2, batch, true, st, -1, data);
+        } else if (one) {  // the whole request in one cooperative launch (ntt_request.cu)
+            ntt::ReqArgs ra;
+            ra.data = data;
+            ra.tf = plan->d_fwd;
+            ra.ti = plan->d_inv;
+            ra.pc = plan->d_pc;
+            ra.bar = gr->bar;
+            ra.L = plan->L;
+            ra.rows = batch * plan->L;
+            ra.flags = flags & 3u;
+            gr->one = true;
+            gr->ra = ra;
+            gr->logn = plan->logn;
+            gr->arith = plan->arith;
+            ek = ntt::launch_request(plan->logn, ra, st, plan->arith);
         } else {
             if (flags & NTT_DIR_FORWARD) ek = enqueue(plan, data, batch, false, st);
             if (ek == cudaSuccess && (flags & NTT_DIR_INVERSE)) ek = enqueue(plan, data, batch, true, st);
@@ -700,9 +746,7 @@ ntt_status_t ntt_graph_create(ntt_graph_t* out, ntt_plan_t plan, uint64_t* data,
     if (st) cudaStreamDestroy(st);
     if (e != cudaSuccess) {
         cudaGetLastError();
-        if (gr->exec) cudaGraphExecDestroy(gr->exec);
-        if (gr->graph) cudaGraphDestroy(gr->graph);
-        delete gr;
+        free_graph(gr);
         return NTT_ERR_CUDA;
     }
     *out = gr;
@@ -712,6 +756,12 @@ ntt_status_t ntt_graph_create(ntt_graph_t* out, ntt_plan_t plan, uint64_t* data,
 ntt_status_t ntt_graph_launch(ntt_graph_t graph, void* stream)
 {
     if (!graph) return NTT_ERR_INVALID_ARG;
+    if (NTT_REQ_DIRECT && graph->one) {
+        DeviceGuard g(graph->device);
+        return ntt::launch_request(graph->logn, graph->ra, (cudaStream_t)stream, graph->arith) == cudaSuccess
+                   ? NTT_OK
+                   : NTT_ERR_CUDA;
+    }
     if (cudaGraphLaunch(graph->exec, (cudaStream_t)stream) != cudaSuccess) {
         cudaGetLastError();
         return NTT_ERR_CUDA;
@@ -724,10 +774,8 @@ ntt_status_t ntt_graph_destroy(ntt_graph_t graph)
     if (!graph) return NTT_OK;
     {
         DeviceGuard g(graph->device);
-        if (graph->exec) cudaGraphExecDestroy(graph->exec);
-        if (graph->graph) cudaGraphDestroy(graph->graph);
+        free_graph(graph);
     }
-    delete graph;
     return NTT_OK;
 }
 

@@ -99,6 +99,20 @@ cudaError_t launch_baseline_forward(int variant, const KArgs& a, cudaStream_t st
 // The paper's "Native" arm: the default forward kernels with native-modulo twiddle products
 // (ntt_native.cu); cudaErrorNotSupported for a non-default split.
 cudaError_t launch_native_forward(KArgs a, uint32_t rows, cudaStream_t st);
+// Single-launch request kernel (ntt_request.cu): forward and / or inverse of
+// rows = batch * L rows of N = 2^14..2^17 in one cooperative launch with grid
+// barriers between the column and block phases.
+struct ReqArgs {
+    uint64_t* data;        // [batch][L][N]
+    const Tw* tf;          // [L][N] Psi, bit-reversed
+    const Tw* ti;          // [L][N] Psi^-1, bit-reversed (R5)
+    const PrimeConst* pc;  // [L]
+    unsigned long long* bar;  // grid barrier arrival counter (kReqBarrierBytes), zeroed once, owned by the request object
+    uint32_t L, rows;      // rows = batch * L
+    uint32_t flags;        // NTT_DIR_FORWARD (1) | NTT_DIR_INVERSE (2)
+};
+constexpr size_t kReqBarrierBytes = 8;  // one 64-bit arrival counter (ntt_request.cu)
+cudaError_t launch_request(unsigned logn, const ReqArgs& a, cudaStream_t st, int arith);
 // 32-bit-word path: all passes of one direction.
 cudaError_t launch32(bool inverse, const KArgs32& a, uint32_t rows, cudaStream_t st);
 }  // namespace ntt

@@ -67,6 +67,19 @@ def test_bench_c5_one_gpu():
     assert set(d["sweep"]) == {"1", "2", "4", "8", "15", "30", "45"}
     for v in d["sweep"].values():
         assert v["latency_us_per_request"] > 0 and v["throughput_us_per_request"] > 0
+        assert set(v["latency_us_by_form"]) == {"graph", "one_kernel"}
+        assert v["latency_us_per_request"] == min(v["latency_us_by_form"].values())
     assert d["roundtrip_exact"] is True
+
+
+def test_bench_c5_two_ranks():
+    """C5 latency mode with the primes of one request sharded over 2 ranks
+    (both request forms, ranks sharing one GPU over gloo)."""
+    _need_gpu()
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
+           "--config", "C5"]
+    d = one_line(subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT))
+    assert d["n_gpus"] == 2 and d["roundtrip_exact"] is True
+    assert d["sweep"]["1"]["latency_primes_per_rank"] == [1, 0]
 
 

@@ -4,6 +4,9 @@ around single launches) and the latency of the request replayed through the
 library's request graph (ntt_graph_create / ntt_graph_launch), per split.
 
     python tools/c5_latency.py [--primes 2n|proth] [--splits 6,7,8,9,10]
+
+The one-kernel request (NTT_GRAPH_ONE_KERNEL, ntt_request.cu) is timed on the
+--splits-one row (its own split does not depend on the plan's).
 """
 import argparse
 import json
@@ -18,7 +21,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import synth  # noqa: E402
-from paper_2012_01968_b200 import NTT_DIR_FORWARD, NTT_DIR_INVERSE, Plan, find_primes  # noqa: E402
+from paper_2012_01968_b200 import NTT_DIR_FORWARD, NTT_DIR_INVERSE, NTT_GRAPH_ONE_KERNEL, Plan, find_primes  # noqa: E402
 
 
 def event_ms(fn, reps=50):
@@ -40,6 +43,7 @@ def main():
     ap.add_argument("--splits", default="6,7,8,9,10")
     ap.add_argument("--L", default="1,8,45")
     ap.add_argument("--logn", type=int, default=16)
+    ap.add_argument("--splits-one", type=int, default=7, help="the split row that also times NTT_GRAPH_ONE_KERNEL")
     args = ap.parse_args()
     N = 1 << args.logn
     for L in [int(v) for v in args.L.split(",")]:
@@ -56,23 +60,26 @@ def main():
                 for p in range(plan.passes):
                     kern[f"{name}_pass{p}_us"] = round(1e3 * event_ms(lambda: plan.launch_pass(x, d, p)), 2)
             x.copy_(ref)
-            g = plan.graph(x, NTT_DIR_FORWARD | NTT_DIR_INVERSE)
-            for _ in range(5):
-                g.launch()
-            lat = 1e3 * event_ms(g.launch, 100)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            e0.record()
-            for _ in range(200):
-                g.launch()
-            e1.record()
-            torch.cuda.synchronize()
-            stream_us = e0.elapsed_time(e1) * 1e3 / 200
-            ok = bool(torch.equal(x, ref))
-            print(json.dumps({"N": N, "L": L, "log_n1": ln1, "primes": args.primes, **kern,
-                              "graph_latency_us": round(lat, 2), "graph_stream_us_per_request": round(stream_us, 2),
-                              "ok": ok}), flush=True)
-            g.close()
+            res = {}
+            for key, fl in (("graph", 0), ("one_kernel", NTT_GRAPH_ONE_KERNEL)):
+                if fl and ln1 != args.splits_one:
+                    continue
+                g = plan.graph(x, NTT_DIR_FORWARD | NTT_DIR_INVERSE | fl)
+                for _ in range(5):
+                    g.launch()
+                lat = 1e3 * event_ms(g.launch, 100)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record()
+                for _ in range(200):
+                    g.launch()
+                e1.record()
+                torch.cuda.synchronize()
+                res[f"{key}_latency_us"] = round(lat, 2)
+                res[f"{key}_stream_us_per_request"] = round(e0.elapsed_time(e1) * 1e3 / 200, 2)
+                res[f"{key}_ok"] = bool(torch.equal(x, ref))
+                g.close()
+            print(json.dumps({"N": N, "L": L, "log_n1": ln1, "primes": args.primes, **kern, **res}), flush=True)
             plan.close()
 
 
