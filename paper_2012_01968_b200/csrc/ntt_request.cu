@@ -81,8 +81,10 @@ struct ReqCfg {
 // release add (after bar.sync) publishes the CTA's writes, its acquire polls
 // (before bar.sync) the other CTAs'.  A barrier that has not opened after
 // ~2^32 cycles traps instead of hanging.  (Measured alternatives, DESIGN.md
-// 5.6: 8 counters on separate L2 slices polled by 8 threads, and fences
-// around relaxed operations, were both slower.)
+// 5.6: 8 counters on separate L2 slices polled by 8 threads, fences around
+// relaxed operations, and one flag per CTA written with st.release and polled
+// by one thread per flag -- no atomics, but G x G acquire loads on hot lines:
+// 2.9-3.4 us per barrier -- were all slower.)
 __device__ __forceinline__ void grid_barrier(unsigned long long* cnt, unsigned G)
 {
     __syncthreads();
