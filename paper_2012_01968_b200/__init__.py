@@ -237,7 +237,7 @@ class Plan:
         """Capture the transforms `flags` of the CUDA tensor x (or, with
         NTT_GRAPH_PRODUCT, the product other <- x * other) into a replayable
         request graph (ntt_graph_create).  | NTT_GRAPH_ONE_KERNEL: the whole
-        request as one cooperative kernel (N = 2^14..2^17, no OT)."""
+        request as one persistent kernel (N = 2^14..2^17, no OT)."""
         return Graph(self, x, flags, other)
 
     def corrupt_twiddle(self, direction: int, l: int, index: int, field: int, mask: int) -> None:

@@ -29,9 +29,14 @@
 #include <atomic>
 #include <type_traits>
 
-// CTAs per SM the forward shared-twiddle Kernel-2 is compiled for (tuning constant)
+// CTAs per SM the forward shared-twiddle Kernel-2 is compiled for (tuning
+// constants, per prime family: measured on C4, profiles/r02h_ab_minb_family.jsonl --
+// general primes 1.340 -> 1.325 ms at 4 (64 registers), Proth 1.249 at 3 vs 1.253 at 4)
 #ifndef NTT_K2_FWD_MINB
-#define NTT_K2_FWD_MINB 3
+#define NTT_K2_FWD_MINB 4
+#endif
+#ifndef NTT_K2_FWD_MINB_P
+#define NTT_K2_FWD_MINB_P 3
 #endif
 
 namespace ntt {
@@ -516,13 +521,19 @@ struct SharedCfg {
     static constexpr int CT = 256;
     static constexpr int NB = CT / TB;  // blocks (ciphertexts) per CTA
     static constexpr size_t SMEM = (size_t)NB * (8u << LOGM) + (sizeof(Tw) << LOGM);
-    // measured on C4: the forward (final reduction, more live values) runs
-    // faster with 85 registers at 3 CTAs/SM, the inverse with 64 at 4
-    static constexpr int MINB = INV ? 4 : NTT_K2_FWD_MINB;
+    // measured on C4: the inverse runs best with 64 registers at 4 CTAs/SM;
+    // the forward (final reduction, more live values) with Proth primes at 3
+    // (80 registers), with general primes at 4
+    template <class PCT>
+    static constexpr int minb()
+    {
+        return INV ? 4 : (std::is_same_v<PCT, PrimeConstP> ? NTT_K2_FWD_MINB_P : NTT_K2_FWD_MINB);
+    }
 };
 
 template <int LOGM, bool INV, int OTS, bool MUL = false, class PCT = PrimeConst, int LE2 = 4>
-__global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>::MINB) k_shared(const KArgs a)
+__global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>::template minb<PCT>())
+    k_shared(const KArgs a)
 {
     using SC = Sched<LOGM, LE2>;
     using CC = SharedCfg<LOGM, INV>;
