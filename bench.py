@@ -14,7 +14,10 @@ primes = the R3 chain (p = 1 mod 2N scanned down from 2^60 - 2N + 1, SURVEY
 Multi-GPU: the rows are independent, so the job shards with no
 data-path collective.  --scaling strong (default): the fixed C4 job (32
 ciphertexts x 60 primes) is split into contiguous prime ranges, one per rank
-(30/30, 15x4, 8/8/8/8/7/7/7/7).  --scaling weak: 32 ciphertexts per GPU.
+(30/30, 15x4, 8/8/8/8/7/7/7/7); at N>1 the line also carries "balanced",
+SURVEY 8(e)'s variant (the prime-major rows split evenly, 240 per rank at
+G=8: whole primes plus at most two partial primes, timed and oracle-checked
+the same way).  --scaling weak: 32 ciphertexts per GPU.
 NCCL (torch.distributed) carries the barriers, the max-over-ranks time and,
 after timing, the per-row checksums that rank 0 checks against the oracle.
 
@@ -202,6 +205,28 @@ def weak_shard(rank: int, G: int, L: int, batch_per_gpu: int) -> dict:
 
 def my_shard(rank: int, G: int, L: int, batch: int, scaling: str = "strong") -> dict:
     return strong_shard(rank, G, L, batch) if scaling == "strong" else weak_shard(rank, G, L, batch)
+
+
+def balanced_pieces(rank: int, G: int, L: int, batch: int) -> list[dict]:
+    """SURVEY 8(e)'s balanced variant of the strong split: the job's L*batch
+    rows in prime-major order (row r = (l, b), l = r // batch), cut into G
+    equal ranges; a rank's range is a run of whole primes (all ciphertexts)
+    plus at most two partial primes (a ciphertext range of one prime) at its
+    ends -- one plan and one buffer per piece.  60 x 32 over 8: 240 rows each."""
+    total = L * batch
+    lo, hi = total * rank // G, total * (rank + 1) // G
+    out, r = [], lo
+    while r < hi:
+        l, b = divmod(r, batch)
+        if b == 0 and hi - r >= batch:
+            n = (hi - r) // batch
+            out.append({"prime_offset": l, "L": n, "batch_offset": 0, "batch": batch})
+            r += n * batch
+        else:
+            end = min(hi, (l + 1) * batch)
+            out.append({"prime_offset": l, "L": 1, "batch_offset": b, "batch": end - r})
+            r = end
+    return out
 
 
 def sample_rows(sh: dict) -> list[tuple[int, int]]:
@@ -464,6 +489,64 @@ def modmuls_per_launch(name: str, rows: int, N: int, logn: int, log_n1: int, pas
     return rows * per_row
 
 
+def balanced_run(D, args, logn, L_total, batch_job, cfg_id):
+    """Time and verify the balanced split (balanced_pieces): every rank runs
+    forward then inverse over its pieces, timed with CUDA events between
+    barriers, max over ranks; per-row checksums of one forward, in global
+    prime-major order, are gathered for rank 0's oracle check."""
+    torch = D.torch
+    import synth
+    from paper_2012_01968_b200 import Plan, find_primes
+
+    N = 1 << logn
+    chain = find_primes(N, L_total, args.primes)
+    pieces = []
+    for pc in balanced_pieces(D.rank, D.world, L_total, batch_job):
+        pr = chain[pc["prime_offset"]: pc["prime_offset"] + pc["L"]]
+        host = torch.empty(pc["batch"] * pc["L"] * N, dtype=torch.int64)
+        synth.rns_rows(pr, pc["batch"], N, config_id=cfg_id, prime_offset=pc["prime_offset"], L_total=L_total,
+                       batch_offset=pc["batch_offset"],
+                       out=host.numpy().view(np.uint64).reshape(pc["batch"], pc["L"], N))
+        pieces.append((pc, Plan(N, pr), host.cuda()))
+    ref = [d.clone() for _, _, d in pieces]
+
+    def step():
+        for _, pl, d in pieces:
+            pl.forward(d)
+        for _, pl, d in pieces:
+            pl.inverse(d)
+
+    for _ in range(args.warmup):
+        step()
+    steps = max(3, args.steps // 2)
+    D.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    mine = e0.elapsed_time(e1) / steps
+    ok = all(bool(torch.equal(d, r)) for (_, _, d), r in zip(pieces, ref))
+    cs = []
+    for pc, pl, d in pieces:  # one forward; checksums in prime-major order
+        pl.forward(d)
+        c = row_checksums_torch(d, pc["batch"], pc["L"], N).view(pc["batch"], pc["L"], 3)
+        cs.append(c.transpose(0, 1).reshape(-1, 3))
+        pl.inverse(d)
+    torch.cuda.synchronize()
+    ok = ok and all(bool(torch.equal(d, r)) for (_, _, d), r in zip(pieces, ref))
+    gathered = D.gather_rows(torch.cat(cs))
+    per_rank = [0.0] * D.world
+    per_rank[D.rank] = mine
+    per_rank = D.allreduce(per_rank, "sum")
+    ok = bool(D.allreduce([float(ok)], "min")[0])
+    for _, pl, _ in pieces:
+        pl.close()
+    return per_rank, ok, gathered, len(pieces)
+
+
 def transform_line(D, args, logn, L_total, batch_job, text):
     """C1-C4: time the job, verify, and build rank 0's line."""
     torch = D.torch
@@ -563,6 +646,11 @@ def transform_line(D, args, logn, L_total, batch_job, text):
     e2e_ok = bool(D.allreduce([float(torch.equal(out_host, host))], "min")[0])
     del ws
 
+    bal = None
+    if world > 1 and args.scaling == "strong":  # SURVEY 8(e)'s balanced variant, reported beside
+        del dev
+        bal = balanced_run(D, args, logn, L_total, batch_job, cfg_id)
+
     if rank != 0:
         plan.close()
         return None
@@ -582,6 +670,35 @@ def transform_line(D, args, logn, L_total, batch_job, text):
             checked += 1
             if not np.array_equal(cs_r[b * shr["L"] + l], want):
                 bad.append([r, shr["batch_offset"] + b, gl])
+
+    balanced = None
+    if bal is not None:
+        per_rank_b, ok_b, gathered_b, _ = bal
+        b_checked, b_bad = 0, []
+        for r in range(world):
+            lo = L_total * batch_job * r // world
+            n_r = L_total * batch_job * (r + 1) // world - lo
+            cs_r = gathered_b[r].numpy()
+            for k in sorted({0, n_r - 1, n_r // 2, (n_r * 7) // 11}):
+                gl, gb = divmod(lo + k, batch_job)
+                x = synth.rns_rows([chain_primes[gl]], 1, N, config_id=cfg_id, prime_offset=gl, L_total=L_total,
+                                   batch_offset=gb)
+                want = row_checksums_np(oracle.ntt_batch(x, [chain_primes[gl]], [chain_psis[gl]], +1))[0]
+                b_checked += 1
+                if not np.array_equal(cs_r[k], want):
+                    b_bad.append([r, gb, gl])
+        ms_b = max(per_rank_b)
+        balanced = {
+            "value": round(ms_b * 1e3 / units, 3), "unit": "us", "ms_per_step": round(ms_b, 4),
+            "per_rank_ms": [round(v, 4) for v in per_rank_b],
+            "imbalance": round(max(per_rank_b) / min(per_rank_b), 4),
+            "shard": f"prime-major rows split {L_total * batch_job // world} per rank: whole primes plus at most two "
+                     "partial primes (one plan and one buffer per piece; SURVEY 8(e) variant)",
+            "pieces_per_rank": [len(balanced_pieces(r, world, L_total, batch_job)) for r in range(world)],
+            "roundtrip_exact": ok_b,
+            "verify": {"rows_checked_vs_oracle": b_checked, "mismatched": b_bad, "verified_rows": b_checked - len(b_bad)},
+        }
+        bad = bad + [["balanced"] + m for m in b_bad]
 
     value_us = ms_step * 1e3 / units
     hbm_peak, peak_kind = peaks()
@@ -707,8 +824,10 @@ def transform_line(D, args, logn, L_total, batch_job, text):
                 "what": "ntt_execute_host: pinned host in -> H2D -> fwd -> inv -> D2H, every rank its shard"},
         "gpu_launches": launches,
         "clocks": clocks,
-        "roundtrip_exact": ok_roundtrip,
+        "roundtrip_exact": ok_roundtrip and (balanced is None or balanced["roundtrip_exact"]),
     }
+    if balanced is not None:
+        line["balanced"] = balanced
     plan.close()
     return line
 

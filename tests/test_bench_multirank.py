@@ -47,6 +47,11 @@ def test_bench_gpus2_self_launch_strong():
     assert d["roundtrip_exact"] is True and d["e2e"]["ok"] is True
     assert len(d["per_rank_ms"]) == 2 and d["imbalance"] >= 1.0
     assert d["value"] > 0 and d["roofline"]["bound"] == "alu" and d["gpu_launches"] > 0
+    # SURVEY 8(e)'s balanced variant (C2: 240 rows -> 120 per rank, a partial prime each side)
+    bal = d["balanced"]
+    assert bal["value"] > 0 and bal["roundtrip_exact"] is True and len(bal["per_rank_ms"]) == 2
+    assert bal["verify"]["verified_rows"] > 0 and bal["verify"]["mismatched"] == []
+    assert bal["pieces_per_rank"] == [2, 2]
 
 
 def test_bench_world2_weak_under_torchrun():

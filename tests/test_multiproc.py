@@ -12,7 +12,7 @@ import pytest
 
 import oracle
 import synth
-from bench import gather_rows, my_shard, prime_ranges, row_checksums_np, sample_rows, shard_grid
+from bench import balanced_pieces, gather_rows, my_shard, prime_ranges, row_checksums_np, sample_rows, shard_grid
 
 
 @pytest.mark.parametrize("G", range(1, 9))
@@ -36,6 +36,32 @@ def test_strong_shards_partition_the_c4_job(G):
     assert sizes == {1: [60], 2: [30, 30], 4: [15] * 4, 8: [8, 8, 8, 8, 7, 7, 7, 7]}.get(G, sizes)
     assert max(sizes) - min(sizes) <= 1 and sum(sizes) == L
     assert [n for _, n in prime_ranges(G, L)] == sizes
+
+
+@pytest.mark.parametrize("G", range(1, 9))
+@pytest.mark.parametrize("L,batch", [(60, 32), (45, 64), (15, 16), (7, 3)])
+def test_balanced_pieces_partition_the_job(G, L, batch):
+    """SURVEY 8(e)'s balanced variant: the prime-major rows split into G equal
+    ranges (240 rows per rank for C4 at G = 8), each a run of whole primes and
+    at most two partial primes; every row exactly once, and the pieces' rows
+    in prime-major order are exactly the rank's range."""
+    seen = set()
+    for r in range(G):
+        pcs = balanced_pieces(r, G, L, batch)
+        rows = []
+        for pc in pcs:
+            assert pc["L"] >= 1 and pc["batch"] >= 1
+            assert pc["L"] == 1 or (pc["batch_offset"] == 0 and pc["batch"] == batch)
+            for l in range(pc["prime_offset"], pc["prime_offset"] + pc["L"]):
+                for b in range(pc["batch_offset"], pc["batch_offset"] + pc["batch"]):
+                    rows.append(l * batch + b)
+        lo, hi = L * batch * r // G, L * batch * (r + 1) // G
+        assert rows == list(range(lo, hi))
+        assert sum(1 for pc in pcs if pc["batch"] < batch) <= 2
+        seen.update(rows)
+    assert seen == set(range(L * batch))
+    if (G, L, batch) == (8, 60, 32):
+        assert all(len(balanced_pieces(r, 8, 60, 32)) <= 3 for r in range(8))
 
 
 def test_checksums_detect_single_word_changes():
