@@ -472,6 +472,12 @@ def timed_steps(D, plan, dev, steps, warmup, flush_l2=False, scratch=None, sampl
         ms = start.elapsed_time(end)
     per_kernel = [statistics.mean(ev[s][j].elapsed_time(ev[s][j + 1]) for s in range(steps)) for j in range(len(seq))]
     names = [("fwd" if d == NTT_DIR_FORWARD else "inv") + f"_pass{p}" for d, p in seq]
+    # median and min of the per-step spans, forward and inverse separately
+    spans = [ev[s][0].elapsed_time(ev[s][-1]) for s in range(steps)]
+    fwd = [ev[s][0].elapsed_time(ev[s][passes]) for s in range(steps)]
+    inv = [ev[s][passes].elapsed_time(ev[s][-1]) for s in range(steps)]
+    D.step_stats = {"step_ms_median": round(statistics.median(spans), 4), "step_ms_min": round(min(spans), 4),
+                    "fwd_ms_median": round(statistics.median(fwd), 4), "inv_ms_median": round(statistics.median(inv), 4)}
     return ms, dict(zip(names, per_kernel)), (sampler.summary() if sampler else None), len(seq) * steps
 
 
@@ -579,6 +585,11 @@ def transform_line(D, args, logn, L_total, batch_job, text):
     info = plan.info()
     ms, kern, clocks, launches = timed_steps(D, plan, dev, args.steps, args.warmup, flush_l2, scratch, True)
     ms_step_rank = ms / args.steps
+    step_stats = D.step_stats
+    l2_warm = None
+    if flush_l2:  # small configs also timed L2-warm (no flush between steps)
+        ms_w, _, _, _ = timed_steps(D, plan, dev, args.steps, 1)
+        l2_warm = max(D.allreduce([ms_w / args.steps], "max"))
 
     # ---- verification (untimed): the roundtrip restored every row; then one
     # forward, per-row checksums gathered to rank 0, checked against the oracle
@@ -769,6 +780,10 @@ def transform_line(D, args, logn, L_total, batch_job, text):
             "dist_backend": D.backend if world > 1 else None,
         },
         "residue_ntts_per_s": round(2 * units * L_total / (ms_step * 1e-3), 1),
+        "step_stats": {**step_stats, "what": "rank 0's per-step CUDA-event spans: median, min, and the forward "
+                                            "(Kernel-1 + Kernel-2) and inverse halves"},
+        "l2_warm": ({"value": round(l2_warm * 1e3 / units, 3), "unit": "us", "ms_per_step": round(l2_warm, 4)}
+                    if l2_warm is not None else None),
         "per_rank_ms": [round(v, 4) for v in per_rank_ms],
         "imbalance": round(max(per_rank_ms) / min(per_rank_ms), 4),
         "verify": {"rows_checked_vs_oracle": checked, "mismatched": bad, "verified_rows": checked - len(bad),
