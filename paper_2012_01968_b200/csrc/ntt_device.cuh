@@ -586,4 +586,44 @@ __device__ __forceinline__ uint32_t swz_at(uint32_t sB)
     }
 }
 
+// The same swizzled element as a SHARED-WINDOW BYTE address, from
+// Pb = smem_addr(block) + 8 sB, the block's byte base already added:
+//   swz_at<KS>(sB) = (sB ^ c) + rest,  c = (KS ^ f) & 0xE,  rest = KS & ~0xE
+// (rest's bits are disjoint from sB's and c's, so the XOR never carries), and
+// with the block base a multiple of 128 bytes (bits 4..6 clear, where 8c
+// lands) smem(sb) + 8 swz_at = (Pb ^ 8c) + 8 rest: one LOP3 per distinct c
+// (at most 8 per round) and an immediate offset -- no per-element add of the
+// block base (which ptxas places on the multiply pipe as IMAD.IADD; measured
+// on C4: Kernel-2' 1.255 -> 1.210 ms, Kernel-2 1.324 -> 1.309 ms,
+// profiles/r02h_ab_swz_bytes.jsonl).
+template <uint32_t KS>
+struct SwzByte {
+    static constexpr uint32_t f = (((KS >> 4) ^ (KS >> 5)) & 7u) << 1;
+    static constexpr uint32_t c = (KS ^ f) & 0xEu;
+    static constexpr uint32_t off = 8u * (KS & ~0xEu);
+    __device__ __forceinline__ static uint32_t base(uint32_t Pb) { return c ? (Pb ^ (8u * c)) : Pb; }
+};
+template <uint32_t OFF>
+__device__ __forceinline__ uint64_t lds64_at(uint32_t a)
+{
+    uint64_t v;
+    asm volatile("ld.shared.u64 %0, [%1+%2];" : "=l"(v) : "r"(a), "n"(OFF) : "memory");
+    return v;
+}
+template <uint32_t OFF>
+__device__ __forceinline__ void lds128_at(uint32_t a, uint64_t& x, uint64_t& y)
+{
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2+%3];" : "=l"(x), "=l"(y) : "r"(a), "n"(OFF) : "memory");
+}
+template <uint32_t OFF>
+__device__ __forceinline__ void sts64_at(uint32_t a, uint64_t v)
+{
+    asm volatile("st.shared.u64 [%0+%1], %2;" ::"r"(a), "n"(OFF), "l"(v) : "memory");
+}
+template <uint32_t OFF>
+__device__ __forceinline__ void sts128_at(uint32_t a, uint64_t x, uint64_t y)
+{
+    asm volatile("st.shared.v2.u64 [%0+%1], {%2, %3};" ::"r"(a), "n"(OFF), "l"(x), "l"(y) : "memory");
+}
+
 }  // namespace ntt

@@ -38,6 +38,11 @@
 #ifndef NTT_K2_FWD_MINB_P
 #define NTT_K2_FWD_MINB_P 3
 #endif
+// shared-twiddle Kernel-2's SMEM exchange addressing: 1 = byte addresses with
+// the block base folded in once per round (SwzByte), 0 = element indices
+#ifndef NTT_K2_SWZ_BYTES
+#define NTT_K2_SWZ_BYTES 1
+#endif
 
 namespace ntt {
 
@@ -574,9 +579,30 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
 
     uint64_t x[16];
     // element (qd, k) of the round at swz_at<elem(qd TB, k)>(swz(elem(tib, 0)))
+    const uint32_t sb_addr = (uint32_t)__cvta_generic_to_shared(sb);  // 128-byte aligned (blocks of 8 M bytes)
     auto s_load = [&](auto ri) {
         using Geo = RoundGeo<LOGM, decltype(ri)::value, LE2>;
         const uint32_t sB = swz(Geo::elem(tib, 0));
+        if constexpr (NTT_K2_SWZ_BYTES) {  // byte addresses: block base folded in once (SwzByte)
+            const uint32_t Pb = sb_addr + 8u * sB;
+            static_for<Geo::GPT>([&](auto qdc) {
+                constexpr int qd = decltype(qdc)::value;
+                if constexpr (Geo::s == 1 && Geo::R >= 2) {
+                    static_for<Geo::R / 2>([&](auto kc) {
+                        constexpr int k = 2 * decltype(kc)::value;
+                        using SW = SwzByte<Geo::elem(qd * TB, k)>;
+                        lds128_at<SW::off>(SW::base(Pb), x[qd * Geo::R + k], x[qd * Geo::R + k + 1]);
+                    });
+                } else {
+                    static_for<Geo::R>([&](auto kc) {
+                        constexpr int k = decltype(kc)::value;
+                        using SW = SwzByte<Geo::elem(qd * TB, k)>;
+                        x[qd * Geo::R + k] = lds64_at<SW::off>(SW::base(Pb));
+                    });
+                }
+            });
+            return;
+        }
         static_for<Geo::GPT>([&](auto qdc) {
             constexpr int qd = decltype(qdc)::value;
             if constexpr (Geo::s == 1 && Geo::R >= 2) {
@@ -597,6 +623,26 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
     auto s_store = [&](auto ri) {
         using Geo = RoundGeo<LOGM, decltype(ri)::value, LE2>;
         const uint32_t sB = swz(Geo::elem(tib, 0));
+        if constexpr (NTT_K2_SWZ_BYTES) {
+            const uint32_t Pb = sb_addr + 8u * sB;
+            static_for<Geo::GPT>([&](auto qdc) {
+                constexpr int qd = decltype(qdc)::value;
+                if constexpr (Geo::s == 1 && Geo::R >= 2) {
+                    static_for<Geo::R / 2>([&](auto kc) {
+                        constexpr int k = 2 * decltype(kc)::value;
+                        using SW = SwzByte<Geo::elem(qd * TB, k)>;
+                        sts128_at<SW::off>(SW::base(Pb), x[qd * Geo::R + k], x[qd * Geo::R + k + 1]);
+                    });
+                } else {
+                    static_for<Geo::R>([&](auto kc) {
+                        constexpr int k = decltype(kc)::value;
+                        using SW = SwzByte<Geo::elem(qd * TB, k)>;
+                        sts64_at<SW::off>(SW::base(Pb), x[qd * Geo::R + k]);
+                    });
+                }
+            });
+            return;
+        }
         static_for<Geo::GPT>([&](auto qdc) {
             constexpr int qd = decltype(qdc)::value;
             if constexpr (Geo::s == 1 && Geo::R >= 2) {
