@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>
 {
     using SC = Sched<LOGN1, LOGE>;
     constexpr int M = SC::M, NR = SC::NR, CT = ColsCfg<LOGN1, LOGE>::CT;
-    extern __shared__ __align__(16) uint64_t sm[];  // [M][16] words, then Tw[M]
+    extern __shared__ __align__(128) uint64_t sm[];  // [M][16] words, then Tw[M]
     Tw* tws = reinterpret_cast<Tw*>(sm + M * 16);
     pdl_trigger();
     pdl_wait();
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(ColsPipeCfg<LOGN1, LOGE>::CT, ColsPipeCfg<LOGN
     using CC = ColsPipeCfg<LOGN1, LOGE>;
     constexpr int M = SC::M, NR = SC::NR, CT = CC::CT;
     constexpr uint32_t logn2 = LOGN - LOGN1;
-    extern __shared__ __align__(16) uint64_t sm[];
+    extern __shared__ __align__(128) uint64_t sm[];  // 128-byte aligned: SwzByte addresses
     pdl_trigger();
     pdl_wait();
     auto tile_of = [&](uint32_t buf) { return sm + buf * (CC::BUF / 8); };
@@ -304,6 +304,91 @@ __global__ void __launch_bounds__(ColsPipeCfg<LOGN1, LOGE>::CT, ColsPipeCfg<LOGN
     asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+// ---------------------------------------------------------------- SMEM round exchange
+// Load / store the thread's groups of round RI from / to a swizzled SMEM block
+// (section 5.3 of DESIGN.md; stride-1 rounds as 128-bit pairs).  When the
+// round's smallest stride s divides TB, elem(qd TB + tib, k) = elem(tib, 0) +
+// elem(qd TB, k) with disjoint bits, so the addresses are SwzByte forms of one
+// per-round base (the block's shared-window byte address folded in once: one
+// LOP3 per distinct swizzle constant, immediate offsets); otherwise (a
+// remainder-first round 0) each element is swizzled on its own.
+template <int LOGM, int LOGE, int RI, int TB>
+__device__ __forceinline__ void xchg_load(uint64_t (&x)[16], const uint64_t* sb, uint32_t tib)
+{
+    using Geo = RoundGeo<LOGM, RI, LOGE>;
+    if constexpr (TB % Geo::s == 0 && LOGM >= 4) {  // blocks of >= 128 bytes: base bits 4..6 clear
+        const uint32_t Pb = (uint32_t)__cvta_generic_to_shared(sb) + 8u * swz(Geo::elem(tib, 0));
+        static_for<Geo::GPT>([&](auto qdc) {
+            constexpr int qd = decltype(qdc)::value;
+            if constexpr (Geo::s == 1 && Geo::R >= 2) {
+                static_for<Geo::R / 2>([&](auto kc) {
+                    constexpr int k = 2 * decltype(kc)::value;
+                    using SW = SwzByte<Geo::elem(qd * TB, k)>;
+                    lds128_at<SW::off>(SW::base(Pb), x[qd * Geo::R + k], x[qd * Geo::R + k + 1]);
+                });
+            } else {
+                static_for<Geo::R>([&](auto kc) {
+                    constexpr int k = decltype(kc)::value;
+                    using SW = SwzByte<Geo::elem(qd * TB, k)>;
+                    x[qd * Geo::R + k] = lds64_at<SW::off>(SW::base(Pb));
+                });
+            }
+        });
+    } else {
+#pragma unroll
+        for (int qd = 0; qd < Geo::GPT; ++qd) {
+            if constexpr (Geo::s == 1 && Geo::R >= 2) {
+#pragma unroll
+                for (int k = 0; k < Geo::R; k += 2) {
+                    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k)));
+                    x[qd * Geo::R + k] = v.x;
+                    x[qd * Geo::R + k + 1] = v.y;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = sb[swz(Geo::elem(qd * TB + tib, k))];
+            }
+        }
+    }
+}
+template <int LOGM, int LOGE, int RI, int TB>
+__device__ __forceinline__ void xchg_store(const uint64_t (&x)[16], uint64_t* sb, uint32_t tib)
+{
+    using Geo = RoundGeo<LOGM, RI, LOGE>;
+    if constexpr (TB % Geo::s == 0 && LOGM >= 4) {  // blocks of >= 128 bytes: base bits 4..6 clear
+        const uint32_t Pb = (uint32_t)__cvta_generic_to_shared(sb) + 8u * swz(Geo::elem(tib, 0));
+        static_for<Geo::GPT>([&](auto qdc) {
+            constexpr int qd = decltype(qdc)::value;
+            if constexpr (Geo::s == 1 && Geo::R >= 2) {
+                static_for<Geo::R / 2>([&](auto kc) {
+                    constexpr int k = 2 * decltype(kc)::value;
+                    using SW = SwzByte<Geo::elem(qd * TB, k)>;
+                    sts128_at<SW::off>(SW::base(Pb), x[qd * Geo::R + k], x[qd * Geo::R + k + 1]);
+                });
+            } else {
+                static_for<Geo::R>([&](auto kc) {
+                    constexpr int k = decltype(kc)::value;
+                    using SW = SwzByte<Geo::elem(qd * TB, k)>;
+                    sts64_at<SW::off>(SW::base(Pb), x[qd * Geo::R + k]);
+                });
+            }
+        });
+    } else {
+#pragma unroll
+        for (int qd = 0; qd < Geo::GPT; ++qd) {
+            if constexpr (Geo::s == 1 && Geo::R >= 2) {
+#pragma unroll
+                for (int k = 0; k < Geo::R; k += 2)
+                    *reinterpret_cast<ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k))) =
+                        make_ulonglong2(x[qd * Geo::R + k], x[qd * Geo::R + k + 1]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < Geo::R; ++k) sb[swz(Geo::elem(qd * TB + tib, k))] = x[qd * Geo::R + k];
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- contiguous
 template <int LOGM, int LOGE, bool TWS = false>
 struct ContigCfg {
@@ -343,7 +428,7 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
     using CC = ContigCfg<LOGM, LOGE, TWS>;
     constexpr int M = SC::M, E = SC::E, TB = SC::TB, NR = SC::NR;
     constexpr int OT_FROM = OTS ? LOGM - OTS : (1 << 20);
-    extern __shared__ __align__(16) uint64_t sm[];
+    extern __shared__ __align__(128) uint64_t sm[];  // 128-byte aligned: SwzByte addresses
     pdl_trigger();
     pdl_wait();
 
@@ -429,39 +514,8 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
             }
         };
         // stride-1 rounds hold adjacent pairs (e, e+1): 128-bit SMEM accesses
-        auto s_load = [&](auto ri) {
-            using Geo = RoundGeo<LOGM, decltype(ri)::value, LOGE>;
-#pragma unroll
-            for (int qd = 0; qd < Geo::GPT; ++qd) {
-                if constexpr (Geo::s == 1 && Geo::R >= 2) {
-#pragma unroll
-                    for (int k = 0; k < Geo::R; k += 2) {
-                        const ulonglong2 v =
-                            *reinterpret_cast<const ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k)));
-                        x[qd * Geo::R + k] = v.x;
-                        x[qd * Geo::R + k + 1] = v.y;
-                    }
-                } else {
-#pragma unroll
-                    for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = sb[swz(Geo::elem(qd * TB + tib, k))];
-                }
-            }
-        };
-        auto s_store = [&](auto ri) {
-            using Geo = RoundGeo<LOGM, decltype(ri)::value, LOGE>;
-#pragma unroll
-            for (int qd = 0; qd < Geo::GPT; ++qd) {
-                if constexpr (Geo::s == 1 && Geo::R >= 2) {
-#pragma unroll
-                    for (int k = 0; k < Geo::R; k += 2)
-                        *reinterpret_cast<ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k))) =
-                            make_ulonglong2(x[qd * Geo::R + k], x[qd * Geo::R + k + 1]);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < Geo::R; ++k) sb[swz(Geo::elem(qd * TB + tib, k))] = x[qd * Geo::R + k];
-                }
-            }
-        };
+        auto s_load = [&](auto ri) { xchg_load<LOGM, LOGE, decltype(ri)::value, TB>(x, sb, tib); };
+        auto s_store = [&](auto ri) { xchg_store<LOGM, LOGE, decltype(ri)::value, TB>(x, sb, tib); };
 
         auto tw_ready = [&]() {};
         if constexpr (!INV) {
@@ -544,7 +598,7 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
     using CC = SharedCfg<LOGM, INV>;
     constexpr int M = SC::M, E = SC::E, TB = SC::TB, NR = SC::NR, NB = CC::NB, CT = CC::CT;
     constexpr int OT_FROM = OTS ? LOGM - OTS : (1 << 20);
-    extern __shared__ __align__(16) uint64_t sm[];
+    extern __shared__ __align__(128) uint64_t sm[];  // 128-byte aligned: SwzByte addresses
     Tw* const tws = reinterpret_cast<Tw*>(sm + NB * M);
     pdl_trigger();
 
@@ -811,7 +865,7 @@ __global__ void __launch_bounds__(PipeCfg<LOGM, LOGE>::CT, PipeCfg<LOGM, LOGE>::
     constexpr int M = SC::M, E = SC::E, TB = SC::TB, NR = SC::NR, NB = PC::NB;
     constexpr int OT_FROM = OTS ? LOGM - OTS : (1 << 20);
     static_assert(TB <= 256 && NB >= 1, "block size");
-    extern __shared__ __align__(16) uint64_t sm[];
+    extern __shared__ __align__(128) uint64_t sm[];  // 128-byte aligned: SwzByte addresses
 
     const uint32_t tid = threadIdx.x, blk = tid / TB, tib = tid % TB;
     const uint32_t n1mask = (1u << a.log_n1) - 1u;
@@ -878,39 +932,8 @@ __global__ void __launch_bounds__(PipeCfg<LOGM, LOGE>::CT, PipeCfg<LOGM, LOGE>::
         };
 
         uint64_t x[16];
-        auto s_load = [&](auto ri) {
-            using Geo = RoundGeo<LOGM, decltype(ri)::value, LOGE>;
-#pragma unroll
-            for (int qd = 0; qd < Geo::GPT; ++qd) {
-                if constexpr (Geo::s == 1 && Geo::R >= 2) {
-#pragma unroll
-                    for (int k = 0; k < Geo::R; k += 2) {
-                        const ulonglong2 v =
-                            *reinterpret_cast<const ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k)));
-                        x[qd * Geo::R + k] = v.x;
-                        x[qd * Geo::R + k + 1] = v.y;
-                    }
-                } else {
-#pragma unroll
-                    for (int k = 0; k < Geo::R; ++k) x[qd * Geo::R + k] = sb[swz(Geo::elem(qd * TB + tib, k))];
-                }
-            }
-        };
-        auto s_store = [&](auto ri) {
-            using Geo = RoundGeo<LOGM, decltype(ri)::value, LOGE>;
-#pragma unroll
-            for (int qd = 0; qd < Geo::GPT; ++qd) {
-                if constexpr (Geo::s == 1 && Geo::R >= 2) {
-#pragma unroll
-                    for (int k = 0; k < Geo::R; k += 2)
-                        *reinterpret_cast<ulonglong2*>(sb + swz(Geo::elem(qd * TB + tib, k))) =
-                            make_ulonglong2(x[qd * Geo::R + k], x[qd * Geo::R + k + 1]);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < Geo::R; ++k) sb[swz(Geo::elem(qd * TB + tib, k))] = x[qd * Geo::R + k];
-                }
-            }
-        };
+        auto s_load = [&](auto ri) { xchg_load<LOGM, LOGE, decltype(ri)::value, TB>(x, sb, tib); };
+        auto s_store = [&](auto ri) { xchg_store<LOGM, LOGE, decltype(ri)::value, TB>(x, sb, tib); };
         auto stage_out = [&]() {
 #pragma unroll
             for (int j = 0; j < E / 2; ++j) {
