@@ -38,11 +38,6 @@
 #ifndef NTT_K2_FWD_MINB_P
 #define NTT_K2_FWD_MINB_P 3
 #endif
-// shared-twiddle Kernel-2's SMEM exchange addressing: 1 = byte addresses with
-// the block base folded in once per round (SwzByte), 0 = element indices
-#ifndef NTT_K2_SWZ_BYTES
-#define NTT_K2_SWZ_BYTES 1
-#endif
 
 namespace ntt {
 
@@ -632,87 +627,9 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
     };
 
     uint64_t x[16];
-    // element (qd, k) of the round at swz_at<elem(qd TB, k)>(swz(elem(tib, 0)))
-    const uint32_t sb_addr = (uint32_t)__cvta_generic_to_shared(sb);  // 128-byte aligned (blocks of 8 M bytes)
-    auto s_load = [&](auto ri) {
-        using Geo = RoundGeo<LOGM, decltype(ri)::value, LE2>;
-        const uint32_t sB = swz(Geo::elem(tib, 0));
-        if constexpr (NTT_K2_SWZ_BYTES) {  // byte addresses: block base folded in once (SwzByte)
-            const uint32_t Pb = sb_addr + 8u * sB;
-            static_for<Geo::GPT>([&](auto qdc) {
-                constexpr int qd = decltype(qdc)::value;
-                if constexpr (Geo::s == 1 && Geo::R >= 2) {
-                    static_for<Geo::R / 2>([&](auto kc) {
-                        constexpr int k = 2 * decltype(kc)::value;
-                        using SW = SwzByte<Geo::elem(qd * TB, k)>;
-                        lds128_at<SW::off>(SW::base(Pb), x[qd * Geo::R + k], x[qd * Geo::R + k + 1]);
-                    });
-                } else {
-                    static_for<Geo::R>([&](auto kc) {
-                        constexpr int k = decltype(kc)::value;
-                        using SW = SwzByte<Geo::elem(qd * TB, k)>;
-                        x[qd * Geo::R + k] = lds64_at<SW::off>(SW::base(Pb));
-                    });
-                }
-            });
-            return;
-        }
-        static_for<Geo::GPT>([&](auto qdc) {
-            constexpr int qd = decltype(qdc)::value;
-            if constexpr (Geo::s == 1 && Geo::R >= 2) {
-                static_for<Geo::R / 2>([&](auto kc) {
-                    constexpr int k = 2 * decltype(kc)::value;
-                    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(sb + swz_at<Geo::elem(qd * TB, k)>(sB));
-                    x[qd * Geo::R + k] = v.x;
-                    x[qd * Geo::R + k + 1] = v.y;
-                });
-            } else {
-                static_for<Geo::R>([&](auto kc) {
-                    constexpr int k = decltype(kc)::value;
-                    x[qd * Geo::R + k] = sb[swz_at<Geo::elem(qd * TB, k)>(sB)];
-                });
-            }
-        });
-    };
-    auto s_store = [&](auto ri) {
-        using Geo = RoundGeo<LOGM, decltype(ri)::value, LE2>;
-        const uint32_t sB = swz(Geo::elem(tib, 0));
-        if constexpr (NTT_K2_SWZ_BYTES) {
-            const uint32_t Pb = sb_addr + 8u * sB;
-            static_for<Geo::GPT>([&](auto qdc) {
-                constexpr int qd = decltype(qdc)::value;
-                if constexpr (Geo::s == 1 && Geo::R >= 2) {
-                    static_for<Geo::R / 2>([&](auto kc) {
-                        constexpr int k = 2 * decltype(kc)::value;
-                        using SW = SwzByte<Geo::elem(qd * TB, k)>;
-                        sts128_at<SW::off>(SW::base(Pb), x[qd * Geo::R + k], x[qd * Geo::R + k + 1]);
-                    });
-                } else {
-                    static_for<Geo::R>([&](auto kc) {
-                        constexpr int k = decltype(kc)::value;
-                        using SW = SwzByte<Geo::elem(qd * TB, k)>;
-                        sts64_at<SW::off>(SW::base(Pb), x[qd * Geo::R + k]);
-                    });
-                }
-            });
-            return;
-        }
-        static_for<Geo::GPT>([&](auto qdc) {
-            constexpr int qd = decltype(qdc)::value;
-            if constexpr (Geo::s == 1 && Geo::R >= 2) {
-                static_for<Geo::R / 2>([&](auto kc) {
-                    constexpr int k = 2 * decltype(kc)::value;
-                    *reinterpret_cast<ulonglong2*>(sb + swz_at<Geo::elem(qd * TB, k)>(sB)) =
-                        make_ulonglong2(x[qd * Geo::R + k], x[qd * Geo::R + k + 1]);
-                });
-            } else {
-                static_for<Geo::R>([&](auto kc) {
-                    constexpr int k = decltype(kc)::value;
-                    sb[swz_at<Geo::elem(qd * TB, k)>(sB)] = x[qd * Geo::R + k];
-                });
-            }
-        });
-    };
+    // round exchanges through the block's swizzled SMEM image (SwzByte addresses)
+    auto s_load = [&](auto ri) { xchg_load<LOGM, LE2, decltype(ri)::value, TB>(x, sb, tib); };
+    auto s_store = [&](auto ri) { xchg_store<LOGM, LE2, decltype(ri)::value, TB>(x, sb, tib); };
     constexpr bool DIRECT0 = RoundGeo<LOGM, 0, LE2>::s >= 16;
     static_assert(DIRECT0, "round 0 is read / written straight from global");
     // remainder-last schedule with a single-stage remainder: the last forward
