@@ -893,6 +893,7 @@ def c5_line(D, args):
         # latency: this rank's prime range of ONE request, replayed from a request graph
         off, n = prime_ranges(world, L)[rank] if world <= L else ((rank, 1) if rank < L else (0, 0))
         forms = {"graph": 0.0, "one_kernel": 0.0}
+        serial = {"graph": 0.0, "one_kernel": 0.0}
         if n > 0:
             lp = Plan(N, primes_all[off: off + n])
             y = torch.empty(n * N, dtype=torch.int64)
@@ -916,7 +917,16 @@ def c5_line(D, args):
                     evs[i + 1].record()
                 torch.cuda.synchronize()
                 forms[form] = statistics.median(evs[i].elapsed_time(evs[i + 1]) for i in range(reps))
-                launches += reps * kernels
+                # the same serial stream with events only at its ends: the per-request
+                # device time without a completion event after every request
+                torch.cuda.synchronize()
+                evs[0].record()
+                for i in range(reps):
+                    g.launch()
+                evs[1].record()
+                torch.cuda.synchronize()
+                serial[form] = evs[0].elapsed_time(evs[1]) / reps
+                launches += 2 * reps * kernels
                 ok_all = ok_all and bool(torch.equal(yd, yref))
                 g.close()
             lp.close()
@@ -924,12 +934,14 @@ def c5_line(D, args):
             D.barrier()
             D.barrier()
         forms = {k: max(D.allreduce([v], "max")) for k, v in sorted(forms.items())}
+        serial = {k: max(D.allreduce([v], "max")) for k, v in sorted(serial.items())}
         lat_form = min(forms, key=forms.get)  # the faster request form at this L
         lat_ms = forms[lat_form]
         sweep[str(L)] = {"throughput_us_per_request": round(tp_ms * 1e3 / C5_REQUESTS, 3),
                          "latency_us_per_request": round(lat_ms * 1e3, 3),
                          "latency_form": lat_form,
                          "latency_us_by_form": {k: round(v * 1e3, 3) for k, v in forms.items()},
+                         "serial_us_by_form": {k: round(v * 1e3, 3) for k, v in serial.items()},
                          "latency_primes_per_rank": [c for _, c in prime_ranges(world, L)] if world <= L
                          else [1 if r < L else 0 for r in range(world)]}
     ok_all = bool(D.allreduce([float(ok_all)], "min")[0])
@@ -944,6 +956,9 @@ def c5_line(D, args):
         "data": "synthetic: seeded splitmix64 residues uniform mod each prime (synth/)",
         "config": {"workload": "C5: mixed ciphertext stream, N=2^16, one request = NTT + iNTT of one ciphertext of "
                                f"L primes, L in {C5_LS}; value = latency mode, mean over the sweep",
+                   "latency_how": "one request in flight (each replay waits for the previous on the stream), CUDA "
+                                  "events after every request, median; serial_us_by_form: the same stream timed "
+                                  "with events only at its ends (no per-request completion event)",
                    "N": N, "requests_per_L_throughput": C5_REQUESTS, "primes": PRIME_TEXT[args.primes],
                    "parallelism": f"x{world}" if world > 1 else "1 GPU"},
         "sweep": sweep,
