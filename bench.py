@@ -892,19 +892,22 @@ def c5_line(D, args):
         tp_plan.close()
         # latency: this rank's prime range of ONE request, replayed from a request graph
         off, n = prime_ranges(world, L)[rank] if world <= L else ((rank, 1) if rank < L else (0, 0))
-        forms = {"graph": 0.0, "one_kernel": 0.0}
-        serial = {"graph": 0.0, "one_kernel": 0.0}
+        forms = {"graph": 0.0, "graph_n1_2^7": 0.0, "one_kernel": 0.0}
+        serial = dict(forms)
         if n > 0:
             lp = Plan(N, primes_all[off: off + n])
+            lp7 = Plan(N, primes_all[off: off + n], log_n1=7)  # the split with the shorter Kernel-1 columns
             y = torch.empty(n * N, dtype=torch.int64)
             synth.rns_rows(primes_all[off: off + n], 1, N, config_id=cfg_id, prime_offset=off, L_total=L,
                            out=y.numpy().view(np.uint64).reshape(1, n, N))
             yd = y.cuda()
             yref = yd.clone()
-            # two request forms: the split's kernels (2 per direction) captured
-            # as a graph, and the one-kernel request (NTT_GRAPH_ONE_KERNEL)
-            for form, flag, kernels in (("graph", 0, 2 * lp.passes), ("one_kernel", NTT_GRAPH_ONE_KERNEL, 1)):
-                g = lp.graph(yd, NTT_DIR_FORWARD | NTT_DIR_INVERSE | flag)
+            # request forms: the split's kernels (2 per direction) captured as a
+            # graph -- the default split (2^8 x 2^8) and 2^7 x 2^9 -- and the
+            # one-kernel request (NTT_GRAPH_ONE_KERNEL)
+            for form, pl, flag, kernels in (("graph", lp, 0, 4), ("graph_n1_2^7", lp7, 0, 4),
+                                            ("one_kernel", lp, NTT_GRAPH_ONE_KERNEL, 1)):
+                g = pl.graph(yd, NTT_DIR_FORWARD | NTT_DIR_INVERSE | flag)
                 for _ in range(max(3, args.warmup)):
                     g.launch()
                 reps = max(20, args.steps * 4)
@@ -930,9 +933,10 @@ def c5_line(D, args):
                 ok_all = ok_all and bool(torch.equal(yd, yref))
                 g.close()
             lp.close()
+            lp7.close()
         else:
-            D.barrier()
-            D.barrier()
+            for _ in range(3):
+                D.barrier()
         forms = {k: max(D.allreduce([v], "max")) for k, v in sorted(forms.items())}
         serial = {k: max(D.allreduce([v], "max")) for k, v in sorted(serial.items())}
         lat_form = min(forms, key=forms.get)  # the faster request form at this L

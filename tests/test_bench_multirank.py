@@ -72,7 +72,7 @@ def test_bench_c5_one_gpu():
     assert set(d["sweep"]) == {"1", "2", "4", "8", "15", "30", "45"}
     for v in d["sweep"].values():
         assert v["latency_us_per_request"] > 0 and v["throughput_us_per_request"] > 0
-        assert set(v["latency_us_by_form"]) == {"graph", "one_kernel"}
+        assert set(v["latency_us_by_form"]) == {"graph", "graph_n1_2^7", "one_kernel"}
         assert v["latency_us_per_request"] == min(v["latency_us_by_form"].values())
     assert d["roundtrip_exact"] is True
 
