@@ -36,12 +36,11 @@ __global__ void __launch_bounds__(256, 4) k_bf(uint64_t* out, const Tw* tw, cons
                     else ct_bf(x[k], x[k + half], w, c, red);
                 }
         }
-        if constexpr (GS) {  // bound the GS values (< 4p + 2^(32+s) after s stages) every 16 stages,
-            if ((it & 3) == 3) {  // less often than the kernels' own final normalisation costs
-#pragma unroll
-                for (int i = 0; i < 16; ++i) x[i] = norm4(csub(x[i], c.p4), c);
-            }
-        }
+        // No periodic normalisation (round 1 bounded the GS values every 16
+        // stages, which put ~2 ALU ops per butterfly into the "ceiling" that the
+        // kernels do not pay -- Kernel-2' then measured above it): the values
+        // may leave the lazy range, which changes no instruction's cost (no
+        // data-dependent branch), and the XOR below keeps the work live.
     }
     uint64_t s = 0;
     for (int i = 0; i < 16; ++i) s ^= x[i];
