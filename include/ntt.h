@@ -120,7 +120,8 @@ ntt_status_t ntt_find_psi(uint64_t p, unsigned n, uint64_t *psi);
  * w_bar = floor(w 2^64 / p) (Algorithm 4; R6), the OT base tables
  * fine[r] = psi^r, coarse[q] = psi^(qB) and their inverses, and
  * N^-1.  The plan owns these allocations.  Synchronous.
- * Errors: INVALID_ARG (plan == NULL, primes == NULL, L == 0, bad options),
+ * Errors: INVALID_ARG (plan == NULL, primes == NULL, L == 0, L > 65535 -- a
+ * grid dimension of the kernels --, bad options),
  * INVALID_N, INVALID_PRIME, CUDA (no device), OOM. */
 ntt_status_t ntt_plan_create(ntt_plan_t *plan, unsigned n, const uint64_t *primes, unsigned L);
 ntt_status_t ntt_plan_create_ex(ntt_plan_t *plan, unsigned n, const uint64_t *primes, unsigned L,

@@ -301,7 +301,7 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
 {
     if (!out) return NTT_ERR_INVALID_ARG;
     *out = nullptr;
-    if (!primes || L == 0) return NTT_ERR_INVALID_ARG;
+    if (!primes || L == 0 || L > 65535) return NTT_ERR_INVALID_ARG;  // L is a grid dimension of the kernels
     if (!pow2_in(n, 1, 17)) return NTT_ERR_INVALID_N;
     ntt_opts_t opts{};
     if (o) opts = *o;

@@ -69,9 +69,9 @@ __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>
     pdl_wait();
 
     const uint32_t tid = threadIdx.x, c = tid & 15u, tib = tid >> 4;
+    // grid (batch x tiles, L): prime-major, no integer division in the prologue
     const uint32_t tile = blockIdx.x & ((1u << a.log_tiles) - 1u);
-    const uint32_t q = blockIdx.x >> a.log_tiles;  // prime-major: q = l * batch + b
-    const uint32_t l = q / a.batch, b = q - l * a.batch;
+    const uint32_t b = blockIdx.x >> a.log_tiles, l = blockIdx.y;
     constexpr uint32_t logn2 = LOGN - LOGN1;  // compile-time stride: immediate offsets
     uint64_t* col = a.data + (((uint64_t)b * a.L + l) << LOGN) + tile * 16u + c;
     const Tw* tab = a.tab + ((uint64_t)l << LOGN);
@@ -598,10 +598,9 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
     pdl_trigger();
 
     const uint32_t tid = threadIdx.x, blk = tid / TB, tib = tid % TB;
-    // CTA -> (l, bb, ciphertext group), prime-major then block position
-    const uint32_t groups = (a.batch + NB - 1) / NB;
-    const uint32_t cg = blockIdx.x % groups, rest = blockIdx.x / groups;
-    const uint32_t bb = rest & ((1u << a.log_n1) - 1u), l = rest >> a.log_n1;
+    // grid (ciphertext groups, block positions, primes): prime-major then
+    // block position, no integer division in the prologue
+    const uint32_t cg = blockIdx.x, bb = blockIdx.y, l = blockIdx.z;
     const uint32_t b = cg * NB + blk;
     const bool active = b < a.batch;
     uint64_t* g = a.data + (((uint64_t)(active ? b : 0) * a.L + l) << a.logn) + ((uint64_t)bb << LOGM);
@@ -939,8 +938,8 @@ cudaError_t launch_cols_t(const KArgs& a, uint32_t rows, cudaStream_t st)
             return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
         }))
         return e;
-    const uint64_t grid = (uint64_t)rows << a.log_tiles;
-    return launch_pdl(fn, dim3((unsigned)grid), dim3(CC::CT), CC::SMEM, st, a);
+    // rows = batch * L (L <= 65535, ntt_plan_create_ex)
+    return launch_pdl(fn, dim3((unsigned)(rows / a.L) << a.log_tiles, a.L), dim3(CC::CT), CC::SMEM, st, a);
 }
 
 template <int LOGM, int LOGE, bool INV, bool FUSE0, int OTS, bool TWS, bool MUL, class PCT>
@@ -987,8 +986,7 @@ cudaError_t launch_shared_t(const KArgs& a, cudaStream_t st)
             return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CC::SMEM);
         }))
         return e;
-    const uint64_t grid = ((uint64_t)a.L << a.log_n1) * ((a.batch + CC::NB - 1) / CC::NB);
-    return launch_pdl(fn, dim3((unsigned)grid), dim3(CC::CT), CC::SMEM, st, a);
+    return launch_pdl(fn, dim3((a.batch + CC::NB - 1) / CC::NB, 1u << a.log_n1, a.L), dim3(CC::CT), CC::SMEM, st, a);
 }
 
 template <int LOGM, bool INV, class PCT, int LE2>
