@@ -429,6 +429,9 @@ template <int LOGM, int LOGE, int RI, int OT_FROM, int NI, bool CANON = false, b
 __device__ __forceinline__ void ct_roundN(uint64_t (&x)[NI][16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
                                           const OtF& otf, const C& c)
 {
+#ifdef NTT_PROBE_NOMATH  // experiment builds only (tools/probe_nomath.sh): memory / exchange floor of a kernel
+    return;
+#endif
     using Geo = RoundGeo<LOGM, RI, LOGE>;
     constexpr int R = Geo::R, S = Geo::S;
 #pragma unroll
@@ -480,6 +483,9 @@ template <int LOGM, int LOGE, int RI, int OT_FROM, bool FUSE0, int NI, class Tab
 __device__ __forceinline__ void gs_roundN(uint64_t (&x)[NI][16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
                                           const OtF& otf, const C& c)
 {
+#ifdef NTT_PROBE_NOMATH
+    return;
+#endif
     using Geo = RoundGeo<LOGM, RI, LOGE>;
     constexpr int R = Geo::R, S = Geo::S;
 #pragma unroll
@@ -549,12 +555,19 @@ __device__ __forceinline__ uint64_t reduce_full(uint64_t x, const PrimeConstP& c
     const uint32_t qp1 = q * (0u - c.m1);  // q p1 (mod 2^32): p1 = -m1
     return csub(x - q - ((uint64_t)qp1 << 32), c.p);
 }
+#ifdef NTT_PROBE_NOMATH
+template <class C>
+__device__ __forceinline__ uint64_t norm8(uint64_t x, const C&) { return x; }
+template <class C>
+__device__ __forceinline__ uint64_t norm4(uint64_t x, const C&) { return x; }
+#else
 template <class C>
 __device__ __forceinline__ uint64_t norm8(uint64_t x, const C& c) { return reduce_full(x, c); }
 // [0,4p) -> [0,p) (inverse outputs): two exact conditional subtractions, all
 // on the ALU pipe -- cheaper than reduce_full where the multiply pipe binds.
 template <class C>
 __device__ __forceinline__ uint64_t norm4(uint64_t x, const C& c) { return csub(csub(x, c.p2), c.p); }
+#endif
 
 // SMEM swizzle for contiguous blocks: XOR word-address bits 1..3 with
 // (bits 4..6 ^ bits 5..7).  16-byte pairs (2i, 2i+1) stay adjacent (vector
