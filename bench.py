@@ -893,7 +893,7 @@ def c5_line(D, args):
         # latency: this rank's prime range of ONE request, replayed from a request graph
         off, n = prime_ranges(world, L)[rank] if world <= L else ((rank, 1) if rank < L else (0, 0))
         forms = {"graph": 0.0, "graph_n1_2^7": 0.0, "one_kernel": 0.0}
-        serial = dict(forms)
+        serial, means = dict(forms), dict(forms)
         if n > 0:
             lp = Plan(N, primes_all[off: off + n])
             lp7 = Plan(N, primes_all[off: off + n], log_n1=7)  # the split with the shorter Kernel-1 columns
@@ -919,7 +919,11 @@ def c5_line(D, args):
                     g.launch()
                     evs[i + 1].record()
                 torch.cuda.synchronize()
-                forms[form] = statistics.median(evs[i].elapsed_time(evs[i + 1]) for i in range(reps))
+                spans = [evs[i].elapsed_time(evs[i + 1]) for i in range(reps)]
+                forms[form] = statistics.median(spans)
+                # the event spans come in steps of the timer's granularity (2.048 us
+                # on the B200 boxes): the mean is the finer estimate of the same latency
+                means[form] = statistics.mean(spans)
                 # the same serial stream with events only at its ends: the per-request
                 # device time without a completion event after every request
                 torch.cuda.synchronize()
@@ -939,12 +943,14 @@ def c5_line(D, args):
                 D.barrier()
         forms = {k: max(D.allreduce([v], "max")) for k, v in sorted(forms.items())}
         serial = {k: max(D.allreduce([v], "max")) for k, v in sorted(serial.items())}
+        means = {k: max(D.allreduce([v], "max")) for k, v in sorted(means.items())}
         lat_form = min(forms, key=forms.get)  # the faster request form at this L
         lat_ms = forms[lat_form]
         sweep[str(L)] = {"throughput_us_per_request": round(tp_ms * 1e3 / C5_REQUESTS, 3),
                          "latency_us_per_request": round(lat_ms * 1e3, 3),
                          "latency_form": lat_form,
                          "latency_us_by_form": {k: round(v * 1e3, 3) for k, v in forms.items()},
+                         "latency_mean_us_by_form": {k: round(v * 1e3, 3) for k, v in means.items()},
                          "serial_us_by_form": {k: round(v * 1e3, 3) for k, v in serial.items()},
                          "latency_primes_per_rank": [c for _, c in prime_ranges(world, L)] if world <= L
                          else [1 if r < L else 0 for r in range(world)]}
@@ -961,7 +967,8 @@ def c5_line(D, args):
         "config": {"workload": "C5: mixed ciphertext stream, N=2^16, one request = NTT + iNTT of one ciphertext of "
                                f"L primes, L in {C5_LS}; value = latency mode, mean over the sweep",
                    "latency_how": "one request in flight (each replay waits for the previous on the stream), CUDA "
-                                  "events after every request, median; serial_us_by_form: the same stream timed "
+                                  "events after every request, median (latency_mean_us_by_form: their mean -- the spans come in steps of "
+                                  "the 2.048 us event granularity); serial_us_by_form: the same stream timed "
                                   "with events only at its ends (no per-request completion event)",
                    "N": N, "requests_per_L_throughput": C5_REQUESTS, "primes": PRIME_TEXT[args.primes],
                    "parallelism": f"x{world}" if world > 1 else "1 GPU"},
