@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-I", os.path.join(ROOT, "include")]
 
-SOURCES = ["ntt_kernels.cu", "ntt_kernels_p.cu", "ntt_k1.cu", "ntt_single.cu", "ntt_native.cu", "ntt_fused.cu", "ntt_request.cu", "ntt32.cu", "ntt_baselines.cu", "ntt_api.cu", "ntt32_api.cu", "params.cpp"]
+SOURCES = ["ntt_kernels.cu", "ntt_kernels_p.cu", "ntt_kernels_d.cu", "ntt_k1.cu", "ntt_single.cu", "ntt_native.cu", "ntt_fused.cu", "ntt_request.cu", "ntt32.cu", "ntt_baselines.cu", "ntt_api.cu", "ntt32_api.cu", "params.cpp"]
 HEADERS = ["ntt_kernels.cuh", "ntt_fused.cuh", "ntt_device.cuh", "ntt_launch.h", "params.h"]
 
 

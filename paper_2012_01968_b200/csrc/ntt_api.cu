@@ -40,6 +40,7 @@ struct ntt_plan_s {
     int loge_k1 = 4, loge_k2 = 9;
     int arith = ntt::kArithGeneral;  // prime-constant type of the kernels (ntt_launch.h)
     bool fused = false;            // single-pass cluster kernel per direction (log_n1 = log2 cluster size)
+    bool dform = false;  // every prime p = 2^60 - d, d < 2^32 (R3 chain): the forward Kernel-2's d-form reduction
 };
 
 namespace {
@@ -154,7 +155,8 @@ cudaError_t two_pass(const ntt_plan_s* plan, KArgs a, uint32_t rows, bool invers
     if (!inverse) {
         if (pass != 1 && (e = ntt::launch_k1(false, plan->loge_k1, a, rows, st, plan->arith)) != cudaSuccess)
             return e;
-        if (pass != 0) e = ntt::launch_k2(false, plan->loge_k2, a, ots, 1, st, plan->arith);
+        const int k2_arith = plan->arith == ntt::kArithGeneral && plan->dform ? ntt::kArithGeneralD : plan->arith;
+        if (pass != 0) e = ntt::launch_k2(false, plan->loge_k2, a, ots, 1, st, k2_arith);
         return e;
     }
     if (pass != 1) {
@@ -384,6 +386,8 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
     const bool special_ok = ((loge_k1 == 4 || loge_k1 == 5) && (loge_k2 == 5 || loge_k2 == 7 || loge_k2 == 9)) || fused;
     p->arith = special_ok && all_proth ? ntt::kArithProth : ntt::kArithGeneral;
     p->fused = fused;
+    p->dform = true;
+    for (unsigned l = 0; l < L; ++l) p->dform = p->dform && ((0 - pr[l]) >> 32) == 0xF0000000ull;
 
     // host tables, one thread per hardware thread over primes
     const uint64_t N = n, NOT = ot_base + N / ot_base;

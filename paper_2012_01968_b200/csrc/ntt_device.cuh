@@ -40,6 +40,14 @@ struct __align__(16) PrimeConst {
 struct PrimeConstP : PrimeConst {
 };
 
+// The same constants, as a type that selects the d-form final reduction of
+// the forward (reduce_full below) for primes p = 2^60 - d with d < 2^32 --
+// every prime of the R3 chain.  Everything else is the general arithmetic.
+// Only the forward shared-twiddle Kernel-2 is instantiated on it
+// (ntt_kernels_d.cu), for plans whose primes all have the form (ntt_api.cu).
+struct PrimeConstD : PrimeConst {
+};
+
 // The same constants, as a type that selects the paper's "Native" comparison
 // arithmetic (fig:native_shoup): every twiddle product is reduced
 // with the native 128-by-64-bit modulo, (unsigned __int128)(b w) % p, instead
@@ -561,6 +569,17 @@ __device__ __forceinline__ uint64_t norm8(uint64_t x, const C&) { return x; }
 template <class C>
 __device__ __forceinline__ uint64_t norm4(uint64_t x, const C&) { return x; }
 #else
+// d-form (PrimeConstD, p = 2^60 - d, d < 2^32): x = q 2^60 + lo60 with
+// q = x >> 60 <= 15 and 2^60 = p + d, so x == lo60 + q d (mod p) and
+//   r = lo60(x) + q d < 2^60 + 15 * 2^32 < 2p   (p > 2^60 - 2^32),
+// one exact conditional subtraction finishes: one IMAD.WIDE (q d with the
+// 64-bit addend lo60) instead of IMAD.HI + IMAD.WIDE + IMAD.  Any word.
+// 2^64 - p = 0xF0000000:d, so d is the low word of c.np.
+__device__ __forceinline__ uint64_t reduce_full(uint64_t x, const PrimeConstD& c)
+{
+    const uint32_t q = (uint32_t)(x >> 60);
+    return csub((x & 0x0FFFFFFFFFFFFFFFull) + (uint64_t)q * (uint32_t)c.np, c.p);
+}
 template <class C>
 __device__ __forceinline__ uint64_t norm8(uint64_t x, const C& c) { return reduce_full(x, c); }
 // [0,4p) -> [0,p) (inverse outputs): two exact conditional subtractions, all

@@ -42,6 +42,9 @@ cudaError_t launch_k2(bool inverse, int loge, const KArgs& a, int ots, uint32_t 
 {
     switch (arith) {
         case kArithProth: return launch_k2_p(inverse, loge, a, ots, iters, st);
+        case kArithGeneralD:
+            if (!inverse) return launch_k2_fwd_d(loge, a, ots, iters, st);
+            return launch_k2_t<PrimeConst>(inverse, loge, a, ots, iters, st);
         default: return launch_k2_t<PrimeConst>(inverse, loge, a, ots, iters, st);
     }
 }

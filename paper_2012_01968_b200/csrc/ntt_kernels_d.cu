@@ -1,0 +1,18 @@
+// ntt_kernels_d.cu -- the forward shared-twiddle Kernel-2 instantiated on
+// PrimeConstD: general arithmetic with the d-form final reduction for primes
+// p = 2^60 - d, d < 2^32 (the R3 chain; ntt_device.cuh reduce_full, DESIGN.md
+// 5.1).  Other Kernel-2 forms (small batches, knobs) keep the general type.
+#include "ntt_kernels.cuh"
+
+namespace ntt {
+
+cudaError_t launch_k2_fwd_d(int loge, const KArgs& a, int ots, uint32_t iters, cudaStream_t st)
+{
+    using namespace detail;
+    const int logm = (int)(a.logn - a.log_n1);
+    if ((loge == 7 || (loge == 9 && logm >= 8)) && a.batch >= (4096u >> logm))
+        return shared_switch<false, PrimeConstD>(logm, a, ots, loge == 9, st, K2Sizes{});
+    return launch_k2_t<PrimeConst>(false, loge, a, ots, iters, st);
+}
+
+}  // namespace ntt

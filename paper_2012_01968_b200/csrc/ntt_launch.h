@@ -70,7 +70,10 @@ cudaError_t launch_pdl(void (*fn)(K), dim3 grid, dim3 block, size_t smem, cudaSt
 // kArithGeneral (PrimeConst, any prime) or kArithProth (PrimeConstP: every
 // prime = 1 mod 2^32); DESIGN.md 5.1.  The Proth form exists for the default
 // kernel variants only (ntt_kernels.cuh).
-enum { kArithGeneral = 0, kArithProth = 1 };
+// kArithGeneralD: general arithmetic, every prime p = 2^60 - d with d < 2^32
+// (the R3 chain); passed for the forward Kernel-2 only, whose final reduction
+// then takes the d-form (PrimeConstD, ntt_kernels_d.cu).
+enum { kArithGeneral = 0, kArithProth = 1, kArithGeneralD = 2 };
 // One kernel per row: contiguous rows of N = 2^logn, N <= 2^13.
 cudaError_t launch_single(bool inverse, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st,
                           int arith = kArithGeneral);
@@ -86,6 +89,7 @@ cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cud
 cudaError_t launch_single_g(bool inverse, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
 cudaError_t launch_single_p(bool inverse, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
 cudaError_t launch_k2_p(bool inverse, int loge, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
+cudaError_t launch_k2_fwd_d(int loge, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
 cudaError_t launch_k1_g(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st);
 cudaError_t launch_k1_p(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st);
 // Single-pass NTT / iNTT, one thread-block cluster per row (N = 2^14..2^17;

@@ -95,6 +95,30 @@ def test_mixed_chain_uses_general_arithmetic():
     assert np.array_equal(to_host(d), oracle.ntt_batch(x.copy(), primes, psis, +1))
 
 
+@pytest.mark.parametrize("logn", [13, 16, 17])
+def test_mixed_chain_shared_kernel_both_normalisations(logn):
+    """General arithmetic with primes of both forms in one launch: R3 primes
+    p = 2^60 - d, d < 2^32 (the d-form final reduction) and a
+    Proth prime below 2^60 - 2^32 (reduce_full); batch 8 runs the
+    shared-twiddle Kernel-2 (and the single-CTA kernel at 2^13), full rows
+    compared with the oracle in both directions."""
+    N = 1 << logn
+    primes = oracle.find_primes(1 << 31, 3)[1:] + oracle.find_primes(N, 2)
+    assert any((2**64 - p) >> 32 != 0xF0000000 for p in primes)
+    assert any((2**64 - p) >> 32 == 0xF0000000 for p in primes)
+    psis = [oracle.find_psi(p, N) for p in primes]
+    plan = Plan(N, primes)
+    assert not plan.info()["proth"]
+    x = synth.rns_rows(primes, 8, N, config_id=29)
+    x[0, :, :] = np.array([p - 1 for p in primes], dtype=np.uint64)[:, None]  # largest residues
+    d = to_dev(x)
+    plan.forward(d)
+    X = oracle.ntt_batch(x.copy(), primes, psis, +1)
+    assert np.array_equal(to_host(d), X)
+    plan.inverse(d)
+    assert np.array_equal(to_host(d), x)
+
+
 @pytest.mark.parametrize("logn", [12, 17])
 def test_proth_edge_rows(logn):
     """zeros, delta_0, delta_{N-1}, all p-1 (largest residues: the lazy bounds)."""
