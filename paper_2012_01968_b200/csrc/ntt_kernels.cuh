@@ -662,9 +662,15 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
                 using Geo = RoundGeo<LOGM, RI, LE2>;
                 if (active) {
 #pragma unroll
-                    for (int qd = 0; qd < Geo::GPT; ++qd)
+                    for (int qd = 0; qd < Geo::GPT; ++qd) {
+#ifdef NTT_K2_ST64  // experiment: two 8-byte stores, no register-quad packing
+                        g[Geo::elem(qd * TB + tib, 0)] = x[2 * qd];
+                        g[Geo::elem(qd * TB + tib, 0) + 1] = x[2 * qd + 1];
+#else
                         *reinterpret_cast<ulonglong2*>(g + Geo::elem(qd * TB + tib, 0)) =
                             make_ulonglong2(x[2 * qd], x[2 * qd + 1]);
+#endif
+                    }
                 }
             } else {
                 s_store(ri);
