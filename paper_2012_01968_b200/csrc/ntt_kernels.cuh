@@ -661,15 +661,20 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
                 // straight to global, lanes contiguous (512 bytes per warp store)
                 using Geo = RoundGeo<LOGM, RI, LE2>;
                 if (active) {
+                    // general / d-form primes: two 8-byte stores per pair (a
+                    // 16-byte store needs the pair in a register quad, ~26
+                    // IMAD.MOV per thread on the multiply pipe; -1.1 % on this
+                    // kernel); Proth primes: 16-byte stores (+0.5 % otherwise)
+                    // -- DESIGN.md 5.4c
 #pragma unroll
                     for (int qd = 0; qd < Geo::GPT; ++qd) {
-#ifdef NTT_K2_ST64  // experiment: two 8-byte stores, no register-quad packing
-                        g[Geo::elem(qd * TB + tib, 0)] = x[2 * qd];
-                        g[Geo::elem(qd * TB + tib, 0) + 1] = x[2 * qd + 1];
-#else
-                        *reinterpret_cast<ulonglong2*>(g + Geo::elem(qd * TB + tib, 0)) =
-                            make_ulonglong2(x[2 * qd], x[2 * qd + 1]);
-#endif
+                        if constexpr (std::is_same_v<PCT, PrimeConstP>) {
+                            *reinterpret_cast<ulonglong2*>(g + Geo::elem(qd * TB + tib, 0)) =
+                                make_ulonglong2(x[2 * qd], x[2 * qd + 1]);
+                        } else {
+                            g[Geo::elem(qd * TB + tib, 0)] = x[2 * qd];
+                            g[Geo::elem(qd * TB + tib, 0) + 1] = x[2 * qd + 1];
+                        }
                     }
                 }
             } else {
