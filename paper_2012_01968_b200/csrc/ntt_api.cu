@@ -159,6 +159,9 @@ cudaError_t two_pass(const ntt_plan_s* plan, KArgs a, uint32_t rows, bool invers
         if (pass != 0) e = ntt::launch_k2(false, plan->loge_k2, a, ots, 1, st, k2_arith);
         return e;
     }
+    // Kernel-1' on PrimeConstD (exact-division N^-1) unless this inverse
+    // carries the NTT-domain product, whose N^-1 is R-scaled (Montgomery)
+    const int k1i_arith = plan->arith == ntt::kArithGeneral && plan->dform && !a.mul_a ? ntt::kArithGeneralD : plan->arith;
     if (pass != 1) {
         e = ntt::launch_k2(true, plan->loge_k2, a, ots, 1, st, plan->arith);
         if (e == cudaErrorNotSupported && a.mul_a) {  // unfused: product kernel, then Kernel-2'
@@ -171,7 +174,7 @@ cudaError_t two_pass(const ntt_plan_s* plan, KArgs a, uint32_t rows, bool invers
         if (e != cudaSuccess) return e;
     }
     a.mul_a = nullptr;
-    if (pass != 0) e = ntt::launch_k1(true, plan->loge_k1, a, rows, st, plan->arith);
+    if (pass != 0) e = ntt::launch_k1(true, plan->loge_k1, a, rows, st, k1i_arith);
     return e;
 }
 
@@ -424,6 +427,9 @@ ntt_status_t ntt_plan_create_ex(ntt_plan_t* out, unsigned n, const uint64_t* pri
                 c.p8 = 8 * q;
                 c.p8_hi = (uint32_t)((8 * q) >> 32);
                 c.zero = 0;
+                c.mN = (q - 1) >> logn;  // div_n (PrimeConstD Kernel-1'); p = 1 mod 2N
+                c.logn = logn;
+                c.nmask = (uint32_t)(N - 1);
                 nttp::Twiddle t1 = nttp::shoup_pair(ninv, q), t2 = nttp::shoup_pair(ninv_psi, q);
                 c.ninv = Tw{t1.w, t1.wb};
                 c.ninv_psi = Tw{t2.w, t2.wb};

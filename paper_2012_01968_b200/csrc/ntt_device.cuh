@@ -16,7 +16,7 @@ struct __align__(16) Tw {
     uint64_t w, wb;
 };
 
-// Per-prime constants, 112 bytes.
+// Per-prime constants, 128 bytes.
 struct __align__(16) PrimeConst {
     uint64_t p, p2, p4;  // p, 2p, 4p
     uint64_t np;         // 2^64 - p
@@ -30,6 +30,8 @@ struct __align__(16) PrimeConst {
     uint32_t p8_hi;      // high word of 8p
     uint64_t p8;         // 8p: Proth primes reduce by 8p on every other stage (ct_bf)
     uint64_t zero;       // 0, opaque to the compiler: a third operand that keeps 64-bit adds on IADD3
+    uint64_t mN;         // (p - 1) / N: the exact-division N^-1 of PrimeConstD (div_n)
+    uint32_t logn, nmask;  // log2 N, N - 1
 };
 
 // The same constants, as a type that selects the Proth-prime arithmetic: for
@@ -43,8 +45,10 @@ struct PrimeConstP : PrimeConst {
 // The same constants, as a type that selects the d-form final reduction of
 // the forward (reduce_full below) for primes p = 2^60 - d with d < 2^32 --
 // every prime of the R3 chain.  Everything else is the general arithmetic.
-// Only the forward shared-twiddle Kernel-2 is instantiated on it
-// (ntt_kernels_d.cu), for plans whose primes all have the form (ntt_api.cu).
+// Kernel-1' takes on it the exact-division form of its fused N^-1 (div_n).
+// Only the forward shared-twiddle Kernel-2 and Kernel-1' are instantiated on
+// it (ntt_kernels_d.cu), for plans whose primes all have the form and not in
+// the NTT-domain product path, whose N^-1 carries a Montgomery factor (ntt_api.cu).
 struct PrimeConstD : PrimeConst {
 };
 
@@ -484,6 +488,33 @@ __device__ __forceinline__ void ct_round(uint64_t (&x)[16], uint32_t tib, uint32
                                                        otf, c);
 }
 
+// x N^-1 mod p as an exact division (the fused N^-1 of the inverse's X'
+// outputs, R15; PrimeConstD plans only): every NTT prime is p = 1 + mN N
+// (p = 1 mod 2N), so with k = -x mod N the sum x + k p =
+// (x + k) + k mN N is divisible by N and
+//   r = (x + k) / N + k mN  ==  x N^-1  (mod p),   r < x / N + p,
+// below 4p for the GS sums x < 8p + 2^50 (N >= 2^14 in Kernel-1'): one
+// IMAD.WIDE + one IMAD (k < N, mN < 2^46) and ALU adds / shifts instead of a
+// Shoup multiply (3 IMAD.WIDE + 2 IMAD.HI + 4 IMAD).
+__device__ __forceinline__ uint64_t div_n(uint64_t x, const PrimeConst& c)
+{
+    const uint32_t k = (0u - (uint32_t)x) & c.nmask;
+    const uint64_t s = (x + k) >> c.logn;
+    uint64_t r;
+    asm("{\n\t"
+        ".reg .u32 m0, m1, r0, r1;\n\t"
+        ".reg .u64 a;\n\t"
+        "mov.b64 {m0, m1}, %2;\n\t"
+        "mad.wide.u32 a, %1, m0, %3;\n\t"
+        "mov.b64 {r0, r1}, a;\n\t"
+        "mad.lo.u32 r1, %1, m1, r1;\n\t"
+        "mov.b64 %0, {r0, r1};\n\t"
+        "}"
+        : "=l"(r)
+        : "r"(k), "l"(c.mN), "l"(s));
+    return r;
+}
+
 // Inverse round: the same groups and twiddle indices, Gentleman-Sande stages
 // in reverse order.  FUSE0: local stage 0 is global stage 0 (m = 1), where
 // N^-1 is fused: X' = (X+Y) N^-1, Y' = (X-Y) Psi^-1[1] N^-1 (R15).
@@ -510,7 +541,11 @@ __device__ __forceinline__ void gs_roundN(uint64_t (&x)[NI][16], uint32_t tib, u
 #pragma unroll
                     for (int n = 0; n < NI; ++n) {
                         const uint64_t u = x[n][qd * R + k], v = x[n][qd * R + k + half];
-                        x[n][qd * R + k] = a.mul(u + v, c);
+                        if constexpr (std::is_same_v<C, PrimeConstD>) {
+                            x[n][qd * R + k] = div_n(u + v, c);
+                        } else {
+                            x[n][qd * R + k] = a.mul(u + v, c);
+                        }
                         x[n][qd * R + k + half] = b.mul(u - v + c.p5, c);
                     }
                 continue;

@@ -71,8 +71,9 @@ cudaError_t launch_pdl(void (*fn)(K), dim3 grid, dim3 block, size_t smem, cudaSt
 // prime = 1 mod 2^32); DESIGN.md 5.1.  The Proth form exists for the default
 // kernel variants only (ntt_kernels.cuh).
 // kArithGeneralD: general arithmetic, every prime p = 2^60 - d with d < 2^32
-// (the R3 chain); passed for the forward Kernel-2 only, whose final reduction
-// then takes the d-form (PrimeConstD, ntt_kernels_d.cu).
+// (the R3 chain); passed for the forward Kernel-2 (d-form final reduction)
+// and for Kernel-1' outside the NTT-domain product path (exact-division N^-1);
+// PrimeConstD, ntt_kernels_d.cu.
 enum { kArithGeneral = 0, kArithProth = 1, kArithGeneralD = 2 };
 // One kernel per row: contiguous rows of N = 2^logn, N <= 2^13.
 cudaError_t launch_single(bool inverse, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st,
@@ -90,6 +91,7 @@ cudaError_t launch_single_g(bool inverse, const KArgs& a, int ot_stages, uint32_
 cudaError_t launch_single_p(bool inverse, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
 cudaError_t launch_k2_p(bool inverse, int loge, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
 cudaError_t launch_k2_fwd_d(int loge, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
+cudaError_t launch_k1_inv_d(int loge, const KArgs& a, uint32_t rows, cudaStream_t st);
 cudaError_t launch_k1_g(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st);
 cudaError_t launch_k1_p(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st);
 // Single-pass NTT / iNTT, one thread-block cluster per row (N = 2^14..2^17;

@@ -212,9 +212,9 @@ def test_golden_table_sizes(golden):
         assert t["psi_bytes"] * g["directions"] == g["bytes"], g["cite"]
     for g in golden["ot_entries"]:
         assert table_sizes(g["N"], 1, g["base"])["ot_entries"] == g["entries"], g["cite"]
-    # a default C4 plan: Psi + Psi^-1, their Kernel-2 copies, OT bases, two 112-byte PrimeConst per prime
+    # a default C4 plan: Psi + Psi^-1, their Kernel-2 copies, OT bases, two 128-byte PrimeConst per prime
     t = table_sizes(1 << 17, 60)
-    assert t["plan_bytes"] == 4 * 60 * (1 << 17) * 16 + 2 * 60 * 1152 * 16 + 2 * 60 * 112
+    assert t["plan_bytes"] == 4 * 60 * (1 << 17) * 16 + 2 * 60 * 1152 * 16 + 2 * 60 * 128
 
 
 def test_execute_host_validates_host_buffers():
