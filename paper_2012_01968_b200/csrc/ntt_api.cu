@@ -161,7 +161,10 @@ cudaError_t two_pass(const ntt_plan_s* plan, KArgs a, uint32_t rows, bool invers
     }
     // Kernel-1' on PrimeConstD (exact-division N^-1) unless this inverse
     // carries the NTT-domain product, whose N^-1 is R-scaled (Montgomery)
-    const int k1i_arith = plan->arith == ntt::kArithGeneral && plan->dform && !a.mul_a ? ntt::kArithGeneralD : plan->arith;
+    const int k1i_arith = a.mul_a                                               ? plan->arith
+                          : plan->arith == ntt::kArithProth                      ? ntt::kArithProthD
+                          : plan->arith == ntt::kArithGeneral && plan->dform ? ntt::kArithGeneralD
+                                                                               : plan->arith;
     if (pass != 1) {
         e = ntt::launch_k2(true, plan->loge_k2, a, ots, 1, st, plan->arith);
         if (e == cudaErrorNotSupported && a.mul_a) {  // unfused: product kernel, then Kernel-2'

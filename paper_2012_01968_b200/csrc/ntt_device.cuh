@@ -41,6 +41,11 @@ struct __align__(16) PrimeConst {
 // all have this form (ntt_api.cu).
 struct PrimeConstP : PrimeConst {
 };
+// Proth arithmetic plus Kernel-1''s exact-division N^-1 (div_n; see
+// PrimeConstD below): the Kernel-1' instantiation of Proth plans outside the
+// NTT-domain product path (ntt_kernels_d.cu).
+struct PrimeConstPD : PrimeConstP {
+};
 
 // The same constants, as a type that selects the d-form final reduction of
 // the forward (reduce_full below) for primes p = 2^60 - d with d < 2^32 --
@@ -457,7 +462,7 @@ __device__ __forceinline__ void ct_roundN(uint64_t (&x)[NI][16], uint32_t tib, u
             // (ct_bf: red 2 for Proth primes, 3 for any other)
             const int red = ((((LOGM - 1 - (S + i) - (FINAL ? 1 : 0)) & 1) || (CANON && S + i < 2))
                                  ? 0
-                                 : (std::is_same_v<C, PrimeConstP> ? 2 : 3));
+                                 : (std::is_base_of_v<PrimeConstP, C> ? 2 : 3));
 #pragma unroll
             for (int h = 0; h < (1 << i); ++h) {
                 const uint32_t idx = (B << i) + h;
@@ -541,7 +546,7 @@ __device__ __forceinline__ void gs_roundN(uint64_t (&x)[NI][16], uint32_t tib, u
 #pragma unroll
                     for (int n = 0; n < NI; ++n) {
                         const uint64_t u = x[n][qd * R + k], v = x[n][qd * R + k + half];
-                        if constexpr (std::is_same_v<C, PrimeConstD>) {
+                        if constexpr (std::is_same_v<C, PrimeConstD> || std::is_same_v<C, PrimeConstPD>) {
                             x[n][qd * R + k] = div_n(u + v, c);
                         } else {
                             x[n][qd * R + k] = a.mul(u + v, c);

@@ -53,6 +53,9 @@ cudaError_t launch_k1(bool inverse, int loge, const KArgs& a, uint32_t rows, cud
 {
     switch (arith) {
         case kArithProth: return launch_k1_p(inverse, loge, a, rows, st);
+        case kArithProthD:
+            if (inverse) return launch_k1_inv_pd(loge, a, rows, st);
+            return launch_k1_p(inverse, loge, a, rows, st);
         case kArithGeneralD:
             if (inverse) return launch_k1_inv_d(loge, a, rows, st);
             return launch_k1_g(inverse, loge, a, rows, st);

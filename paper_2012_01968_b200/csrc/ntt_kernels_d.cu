@@ -25,4 +25,13 @@ cudaError_t launch_k1_inv_d(int loge, const KArgs& a, uint32_t rows, cudaStream_
     return cols_switch<4, true, PrimeConstD>((int)((a.logn << 4) | a.log_n1), a, rows, st, K1Pairs{});
 }
 
+// Proth plans: Kernel-1' with the exact-division N^-1 on the Proth arithmetic
+cudaError_t launch_k1_inv_pd(int loge, const KArgs& a, uint32_t rows, cudaStream_t st)
+{
+    using namespace detail;
+    if (loge == 5 && a.log_n1 <= 9)
+        return launch_k1_t<PrimeConstP>(true, loge, a, rows, st);
+    return cols_switch<4, true, PrimeConstPD>((int)((a.logn << 4) | a.log_n1), a, rows, st, K1Pairs{});
+}
+
 }  // namespace ntt

@@ -74,7 +74,8 @@ cudaError_t launch_pdl(void (*fn)(K), dim3 grid, dim3 block, size_t smem, cudaSt
 // (the R3 chain); passed for the forward Kernel-2 (d-form final reduction)
 // and for Kernel-1' outside the NTT-domain product path (exact-division N^-1);
 // PrimeConstD, ntt_kernels_d.cu.
-enum { kArithGeneral = 0, kArithProth = 1, kArithGeneralD = 2 };
+// kArithProthD: Proth arithmetic with Kernel-1''s exact-division N^-1 (PrimeConstPD).
+enum { kArithGeneral = 0, kArithProth = 1, kArithGeneralD = 2, kArithProthD = 3 };
 // One kernel per row: contiguous rows of N = 2^logn, N <= 2^13.
 cudaError_t launch_single(bool inverse, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st,
                           int arith = kArithGeneral);
@@ -92,6 +93,7 @@ cudaError_t launch_single_p(bool inverse, const KArgs& a, int ot_stages, uint32_
 cudaError_t launch_k2_p(bool inverse, int loge, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
 cudaError_t launch_k2_fwd_d(int loge, const KArgs& a, int ot_stages, uint32_t iters, cudaStream_t st);
 cudaError_t launch_k1_inv_d(int loge, const KArgs& a, uint32_t rows, cudaStream_t st);
+cudaError_t launch_k1_inv_pd(int loge, const KArgs& a, uint32_t rows, cudaStream_t st);
 cudaError_t launch_k1_g(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st);
 cudaError_t launch_k1_p(bool inverse, int loge, const KArgs& a, uint32_t rows, cudaStream_t st);
 // Single-pass NTT / iNTT, one thread-block cluster per row (N = 2^14..2^17;
