@@ -295,10 +295,17 @@ __device__ __forceinline__ void ct_bf(uint64_t& X, uint64_t& Y, const W& w, cons
 // below 4p + E the carry-free test below subtracts only when x + y > 4p and
 // leaves x + y < 4p + 2^33 otherwise, so E' = max(2E, 2^33).
 //   X' = (X + Y) mod* 4p;  Y' = (X - Y + 5p) w  (5p > any Y, so no wrap).
+// red = false: inputs below 2p (the first stage of an inverse whose input is
+// canonical, or a Montgomery product < 2p), so X + Y < 4p needs no test.
 template <class W, class C>
-__device__ __forceinline__ void gs_bf(uint64_t& X, uint64_t& Y, const W& w, const C& c)
+__device__ __forceinline__ void gs_bf(uint64_t& X, uint64_t& Y, const W& w, const C& c, bool red = true)
 {
     const uint64_t x = X, y = Y;
+    if (!red) {
+        X = x + y + c.zero;  // three inputs: IADD3 / IADD3.X
+        Y = w.mul(x - y + c.p5, c);
+        return;
+    }
     // subtract 4p iff hi(x) + hi(y) > hi(4p): a carry-free test, so X' is
     // one 3-input add (see ct_bf)
     const bool ge = (uint32_t)(x >> 32) + (uint32_t)(y >> 32) > c.p4_hi;
@@ -523,7 +530,10 @@ __device__ __forceinline__ uint64_t div_n(uint64_t x, const PrimeConst& c)
 // Inverse round: the same groups and twiddle indices, Gentleman-Sande stages
 // in reverse order.  FUSE0: local stage 0 is global stage 0 (m = 1), where
 // N^-1 is fused: X' = (X+Y) N^-1, Y' = (X-Y) Psi^-1[1] N^-1 (R15).
-template <int LOGM, int LOGE, int RI, int OT_FROM, bool FUSE0, int NI, class TabF, class OtF, class C>
+// CANON: the sub-transform's input is below 2p, so its first GS stage (local
+// stage LOGM - 1) skips the reduction of X + Y (gs_bf red = false).
+template <int LOGM, int LOGE, int RI, int OT_FROM, bool FUSE0, int NI, bool CANON = false, class TabF, class OtF,
+          class C>
 __device__ __forceinline__ void gs_roundN(uint64_t (&x)[NI][16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
                                           const OtF& otf, const C& c)
 {
@@ -563,13 +573,15 @@ __device__ __forceinline__ void gs_roundN(uint64_t (&x)[NI][16], uint32_t tib, u
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
 #pragma unroll
-                        for (int n = 0; n < NI; ++n) gs_bf(x[n][qd * R + k], x[n][qd * R + k + half], w, c);
+                        for (int n = 0; n < NI; ++n)
+                            gs_bf(x[n][qd * R + k], x[n][qd * R + k + half], w, c, !(CANON && S + i == LOGM - 1));
                 } else {
                     const TwMul<false> w{tabf(TwKey{idx, S + i, S, i, h, G / Geo::s})};
 #pragma unroll
                     for (int k = h * 2 * half; k < h * 2 * half + half; ++k)
 #pragma unroll
-                        for (int n = 0; n < NI; ++n) gs_bf(x[n][qd * R + k], x[n][qd * R + k + half], w, c);
+                        for (int n = 0; n < NI; ++n)
+                            gs_bf(x[n][qd * R + k], x[n][qd * R + k + half], w, c, !(CANON && S + i == LOGM - 1));
                 }
             }
         }
@@ -577,11 +589,12 @@ __device__ __forceinline__ void gs_roundN(uint64_t (&x)[NI][16], uint32_t tib, u
 }
 
 // Inverse round, one sub-transform per thread.
-template <int LOGM, int LOGE, int RI, int OT_FROM, bool FUSE0, class TabF, class OtF, class C>
+template <int LOGM, int LOGE, int RI, int OT_FROM, bool FUSE0, bool CANON = false, class TabF, class OtF, class C>
 __device__ __forceinline__ void gs_round(uint64_t (&x)[16], uint32_t tib, uint32_t Fm1, const TabF& tabf,
                                          const OtF& otf, const C& c)
 {
-    gs_roundN<LOGM, LOGE, RI, OT_FROM, FUSE0, 1>(reinterpret_cast<uint64_t(&)[1][16]>(x), tib, Fm1, tabf, otf, c);
+    gs_roundN<LOGM, LOGE, RI, OT_FROM, FUSE0, 1, CANON>(reinterpret_cast<uint64_t(&)[1][16]>(x), tib, Fm1, tabf, otf,
+                                                         c);
 }
 
 // Canonical reduction at the end of a direction, for any x < 2^64:

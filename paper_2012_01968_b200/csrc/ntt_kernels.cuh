@@ -708,7 +708,9 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
             constexpr int RI = NR - 1 - decltype(rj)::value;
             using RC = std::integral_constant<int, RI>;
             s_load(RC{});
-            gs_round<LOGM, LE2, RI, OT_FROM, false>(x, tib, Fm1, tabf, otf, pc);
+            // the inverse's input is canonical (or a Montgomery product < 2p):
+            // its first GS stage needs no reduction
+            gs_round<LOGM, LE2, RI, OT_FROM, false, RI == NR - 1>(x, tib, Fm1, tabf, otf, pc);
             if constexpr (RI > 0) {
                 s_store(RC{});
                 block_sync<TB>(blk);
@@ -745,7 +747,9 @@ __global__ void __launch_bounds__(SharedCfg<LOGM, INV>::CT, SharedCfg<LOGM, INV>
             } else {
                 s_load(RC{});
             }
-            gs_round<LOGM, LE2, RI, OT_FROM, false>(x, tib, Fm1, tabf, otf, pc);
+            // the inverse's input is canonical (or a Montgomery product < 2p):
+            // its first GS stage needs no reduction
+            gs_round<LOGM, LE2, RI, OT_FROM, false, RI == NR - 1>(x, tib, Fm1, tabf, otf, pc);
             if constexpr (RI > 0) {
                 s_store(RC{});
                 block_sync<TB>(blk);
