@@ -557,7 +557,11 @@ __device__ __forceinline__ void gs_roundN(uint64_t (&x)[NI][16], uint32_t tib, u
                     for (int n = 0; n < NI; ++n) {
                         const uint64_t u = x[n][qd * R + k], v = x[n][qd * R + k + half];
                         if constexpr (std::is_same_v<C, PrimeConstD> || std::is_same_v<C, PrimeConstPD>) {
-                            x[n][qd * R + k] = div_n(u + v, c);
+                            // canonical outputs here: div_n's r < x/N + p needs one
+                            // subtraction, not norm4's two (Kernel-1' then skips norm4)
+                            x[n][qd * R + k] = csub(div_n(u + v, c), c.p);
+                            x[n][qd * R + k + half] = norm4(b.mul(u - v + c.p5, c), c);
+                            continue;
                         } else {
                             x[n][qd * R + k] = a.mul(u + v, c);
                         }

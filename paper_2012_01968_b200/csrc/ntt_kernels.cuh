@@ -154,8 +154,11 @@ __global__ void __launch_bounds__(ColsCfg<LOGN1, LOGE>::CT, ColsCfg<LOGN1, LOGE>
             }
             gs_round<LOGN1, LOGE, RI, 1 << 20, true>(x, tib, 0u, tabf, otf, pc);
             if constexpr (RI == 0) {
+                // PrimeConstD / PD: the fused last stage already left canonical words
+                if constexpr (!(std::is_same_v<PCT, PrimeConstD> || std::is_same_v<PCT, PrimeConstPD>)) {
 #pragma unroll
-                for (int k = 0; k < SC::E; ++k) x[k] = norm4(x[k], pc);  // canonical [0, p)
+                    for (int k = 0; k < SC::E; ++k) x[k] = norm4(x[k], pc);  // canonical [0, p)
+                }
                 g_store(RC{});
             } else {
                 s_store(RC{});
