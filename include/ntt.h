@@ -140,13 +140,19 @@ ntt_status_t ntt_plan_info(ntt_plan_t plan, unsigned *L, unsigned *logn, unsigne
 
 /* ntt_plan_exec -- host query of how the plan executes (any output may be NULL):
  * *arith   = the Shoup arithmetic the kernels run (ntt_opts_t.prime_arith):
- *            NTT_ARITH_GENERAL or NTT_ARITH_PROTH (every prime = 1 mod 2^32);
+ *            NTT_ARITH_GENERAL, NTT_ARITH_PROTH (every prime = 1 mod 2^32),
+ *            or NTT_ARITH_GENERAL_D: the general arithmetic with every prime
+ *            p = 2^60 - d, d < 2^32 (e.g. the chain ntt_find_primes scans), where
+ *            the forward Kernel-2's final reduction takes the d-form and
+ *            Kernel-1' applies N^-1 as an exact division;
+ *            results are identical in every case;
  * *passes  = kernels per direction (1: single CTA or single-pass cluster
  *            kernel; 2: the paper's two-kernel split);
  * *cluster = CTAs per row of the single-pass cluster kernel (N / 2^13), 1 if
  *            it is not used. */
 #define NTT_ARITH_GENERAL 0
 #define NTT_ARITH_PROTH 1
+#define NTT_ARITH_GENERAL_D 2
 ntt_status_t ntt_plan_exec(ntt_plan_t plan, int *arith, unsigned *passes, unsigned *cluster);
 
 /* ntt_forward -- in-place forward merged negacyclic NTT of batch*L rows.

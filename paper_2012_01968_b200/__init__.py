@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import ctypes
 
-from ._native import (NTT_ARITH_PROTH, NTT_DIR_FORWARD, NTT_DIR_INVERSE, NTT_GRAPH_ONE_KERNEL, NTT_GRAPH_PRODUCT,
+from ._native import (NTT_ARITH_GENERAL_D, NTT_ARITH_PROTH, NTT_DIR_FORWARD, NTT_DIR_INVERSE, NTT_GRAPH_ONE_KERNEL, NTT_GRAPH_PRODUCT,
                       NTT_PRIMES_2N,
                       NTT_PRIMES_PROTH32, NttError, Opts, check, lib)
 
@@ -160,7 +160,8 @@ class Plan:
         check(lib().ntt_plan_exec(self.handle, ctypes.byref(pr), ctypes.byref(npass), ctypes.byref(ncl)))
         return {"L": L.value, "logn": logn.value, "log_n1": logn1.value, "ot_enable": bool(ote.value),
                 "ot_base": otb.value, "ot_stages": ots.value, "table_bytes": tb.value,
-                "proth": pr.value == NTT_ARITH_PROTH, "arith": "proth" if pr.value == NTT_ARITH_PROTH else "general",
+                "proth": pr.value == NTT_ARITH_PROTH,
+                "arith": {NTT_ARITH_PROTH: "proth", NTT_ARITH_GENERAL_D: "general-d"}.get(pr.value, "general"),
                 "passes": npass.value, "cluster": ncl.value}
 
     # ---------------------------------------------------------------- transforms

@@ -19,7 +19,7 @@ NTT_DIR_FORWARD = 1
 NTT_DIR_INVERSE = 2
 NTT_VARIANT_DEFAULT, NTT_VARIANT_RADIX2, NTT_VARIANT_RADIX16, NTT_VARIANT_NATIVE = 0, 1, 2, 3
 NTT_PRIMES_2N, NTT_PRIMES_PROTH32 = 0, 1
-NTT_ARITH_GENERAL, NTT_ARITH_PROTH = 0, 1
+NTT_ARITH_GENERAL, NTT_ARITH_PROTH, NTT_ARITH_GENERAL_D = 0, 1, 2
 NTT_GRAPH_PRODUCT = 4
 NTT_GRAPH_ONE_KERNEL = 8
 

@@ -521,7 +521,7 @@ ntt_status_t ntt_plan_info(ntt_plan_t plan, unsigned* L, unsigned* logn, unsigne
 ntt_status_t ntt_plan_exec(ntt_plan_t plan, int* arith, unsigned* passes, unsigned* cluster)
 {
     if (!plan) return NTT_ERR_INVALID_ARG;
-    if (arith) *arith = plan->arith;
+    if (arith) *arith = plan->arith == ntt::kArithGeneral && plan->dform ? ntt::kArithGeneralD : plan->arith;
     if (passes) *passes = (plan->fused || plan->log_n1 == 0) ? 1u : 2u;
     if (cluster) *cluster = plan->fused ? (1u << plan->log_n1) : 1u;
     return NTT_OK;

@@ -95,6 +95,14 @@ def test_mixed_chain_uses_general_arithmetic():
     assert np.array_equal(to_host(d), oracle.ntt_batch(x.copy(), primes, psis, +1))
 
 
+def test_plan_reports_the_d_form_arithmetic():
+    """R3 chains (every prime 2^60 - d, d < 2^32) run the PrimeConstD kernels;
+    Proth chains the Proth ones (ntt_plan_exec, ntt.h)."""
+    N = 1 << 17
+    assert Plan(N, oracle.find_primes(N, 4)).info()["arith"] == "general-d"
+    assert Plan(N, oracle.find_primes(1 << 31, 4)).info()["arith"] == "proth"
+
+
 @pytest.mark.parametrize("logn", [13, 16, 17])
 def test_mixed_chain_shared_kernel_both_normalisations(logn):
     """General arithmetic with primes of both forms in one launch: R3 primes
@@ -108,7 +116,7 @@ def test_mixed_chain_shared_kernel_both_normalisations(logn):
     assert any((2**64 - p) >> 32 == 0xF0000000 for p in primes)
     psis = [oracle.find_psi(p, N) for p in primes]
     plan = Plan(N, primes)
-    assert not plan.info()["proth"]
+    assert plan.info()["arith"] == "general"  # not every prime is 2^60 - d, d < 2^32
     x = synth.rns_rows(primes, 8, N, config_id=29)
     x[0, :, :] = np.array([p - 1 for p in primes], dtype=np.uint64)[:, None]  # largest residues
     d = to_dev(x)
