@@ -393,7 +393,12 @@ struct ContigCfg {
     static constexpr int TB = Sched<LOGM, LOGE>::TB;
     static constexpr int CT = TB > 256 ? TB : 256;  // threads per CTA
     static constexpr int NB = CT / TB;              // blocks per CTA iteration
-    static constexpr size_t SMEM = (size_t)NB * (1 << LOGM) * 8;  // data words
+    // TWP: a one-row-per-CTA single kernel at N = 2^12 (C1) copies its row's
+    // whole Psi table into SMEM with cp.async at the start, overlapped with the
+    // data loads, instead of loading each round's twiddles from L2 when the
+    // round starts (a latency the one CTA cannot hide)
+    static constexpr bool TWP = !TWS && NB == 1 && LOGM == 12;
+    static constexpr size_t SMEM = (size_t)NB * (1 << LOGM) * 8 + (TWP ? (size_t)(1 << LOGM) * 16 : 0);
     // register budget: the Kernel-2 mode (TWS) targets 32 warps/SM like Kernel-1
     static constexpr int MINB = CT > 256 ? 1 : (TWS ? 3 : (LOGE >= 4 ? 2 : 3));
 };
@@ -449,9 +454,16 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
         // TWS (Kernel-2 mode): twiddles from the plan's Kernel-2 table, whose
         // per-round [i][h][g] order makes every warp read contiguous entries.
         const Tw* tb2 = a.tab2 + ((uint64_t)l << a.logn) + ((uint64_t)bb << LOGM);
+        Tw* const twp = reinterpret_cast<Tw*>(sm + CC::NB * M);  // CC::TWP: the row's Psi table
+        if constexpr (CC::TWP) {
+            for (uint32_t i = tid; i < (uint32_t)M; i += CC::CT) cp_async16(twp + i, tab + i);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
         auto tabf = [&](const TwKey& k) {
             if constexpr (TWS) {
                 return ldg_tw(tb2 + K2Layout<LOGM, LOGE>::round_off(k.S) + ((((1u << k.i) - 1u + k.h) << k.S) + k.g));
+            } else if constexpr (CC::TWP) {
+                return twp[k.idx + ((F - 1u) << k.j)];
             } else {
                 return ldg_tw(tab + k.idx + ((F - 1u) << k.j));
             }
@@ -515,7 +527,12 @@ __global__ void __launch_bounds__(ContigCfg<LOGM, LOGE, TWS>::CT, ContigCfg<LOGM
         auto s_load = [&](auto ri) { xchg_load<LOGM, LOGE, decltype(ri)::value, TB>(x, sb, tib); };
         auto s_store = [&](auto ri) { xchg_store<LOGM, LOGE, decltype(ri)::value, TB>(x, sb, tib); };
 
-        auto tw_ready = [&]() {};
+        auto tw_ready = [&]() {
+            if constexpr (CC::TWP) {
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                __syncthreads();
+            }
+        };
         if constexpr (!INV) {
             if constexpr (!DIRECT0) stage_in();
             tw_ready();
